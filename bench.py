@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path.
+
+One "step" = one call of the kernel entry point (C ABI) over one batch of
+synthetic input with BASELINE.json's shapes.  Default workload: BASELINE
+configs[1] (config 2, SpAdd D = A+B+C, 3 x 200k x 200k, 50/row); ``--config``
+selects any of the five.
+
+Our arm (default):
+  value    = algorithmic HBM bytes of the call (inputs read once + output written
+             once, int64 indices / fp64 values) / device time per step, with the
+             inputs resident in HBM; whole-job aggregate over ranks.
+  e2e      = the same metric through the same C-ABI call with pinned HOST
+             inputs and a HOST result (H2D + D2H inside the timed region).
+  roofline = dominant kernel's algorithmic bytes / its CUDA-event duration vs
+             the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline = the reference CPU path (oracle/_ref: the reference's own
+             Workspace/TensorBuilder) on the host cores, bounded sample.
+
+``--impl reference``: rank 0 times the reference CPU path alone on the same
+config/metric (other ranks exit), printing the same JSON line.
+
+Multi-GPU (torchrun): weak scaling — every rank processes its own full-size
+shard of the row (slice) dimension with independently seeded inputs; no
+collective on the data path; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SpGEMM/SpAdd/MTTKRP useful GFLOP/s; achieved HBM GB/s vs B200 peak"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+
+
+def _peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def _traffic(workload: str, kernel: str):
+    """DRAM bytes per launch from a committed `ncu --set full` capture."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def _csr_bytes(m) -> int:
+    return 8 * (m.nrows + 1) + 16 * m.nnz
+
+
+def _csf_bytes(b) -> int:
+    return 8 * (b.dims[0] + 1) + 8 * b.nfibers + 8 * (b.nfibers + 1) + 16 * b.nnz
+
+
+class Workload:
+    """Common driver: inputs on device, raw C-ABI step, e2e step, CPU ref."""
+
+    def __init__(self, cid: int, shard: int):
+        from paper_1802_10574_b200 import generators as G
+
+        self.cid = cid
+        self.name = G.CONFIG_NAMES[cid]
+        t = time.time()
+        self.cfg = G.make_config(cid, shard=shard)
+        self.gen_s = time.time() - t
+
+    # populated by subclasses
+    def setup(self, ctx):
+        raise NotImplementedError
+
+    def step(self, timing=False):
+        raise NotImplementedError
+
+    def e2e_step(self):
+        raise NotImplementedError
+
+
+class SpaddWork(Workload):
+    def setup(self, ctx):
+        from paper_1802_10574_b200 import _native as N
+
+        self.N = N
+        self.ctx = ctx
+        self.lib = N.load()
+        self.dev = [o.to("cuda") for o in self.cfg["ops"]]
+        self.views = (N.CsrView * len(self.dev))(*[o.view() for o in self.dev])
+        import torch
+
+        self.pinned = []
+        for o in self.cfg["ops"]:
+            arrs = [torch.from_numpy(a).pin_memory() for a in (o.pos, o.idx, o.vals)]
+            self.pinned.append(arrs)
+        from paper_1802_10574_b200.storage import CSR
+
+        hops = [CSR(o.nrows, o.ncols, *arrs) for o, arrs in zip(self.cfg["ops"], self.pinned)]
+        self.hviews = (N.CsrView * len(hops))(*[h.view() for h in hops])
+        for v in self.hviews:
+            v.mem = N.STAM_MEM_HOST
+        self.in_bytes = sum(_csr_bytes(o) for o in self.cfg["ops"])
+        self.nnz_out = None
+
+    def _call(self, views, result_mem, timing):
+        N = self.N
+        r = N.CsrResult()
+        st = N.Stats()
+        opts = N.Options(1, 0, result_mem, 1 if timing else 0)
+        N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.dev), views, C.byref(opts),
+                                         C.byref(r), C.byref(st)))
+        nnz, nrows = r.nnz, r.nrows
+        N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
+        self.nnz_out = nnz
+        self.out_bytes = 8 * (nrows + 1) + 16 * nnz
+        return st
+
+    def step(self, timing=False):
+        return self._call(self.views, self.N.STAM_MEM_DEVICE, timing)
+
+    def e2e_step(self):
+        return self._call(self.hviews, self.N.STAM_MEM_HOST, False)
+
+    def algo_bytes(self):
+        return self.in_bytes + self.out_bytes
+
+    def flops(self):
+        # workspace adds executed (SPEC counters: every accumulate insert)
+        return sum(o.nnz for o in self.cfg["ops"][1:])
+
+    def h2d_bytes(self):
+        return self.in_bytes
+
+    def d2h_bytes(self):
+        return self.out_bytes
+
+    # reference CPU path on a row sample
+    def ref_sample(self, rows):
+        import numpy as np
+        from paper_1802_10574_b200.storage import CSR
+
+        sub = []
+        for o in self.cfg["ops"]:
+            e = int(o.pos[rows])
+            sub.append(CSR(rows, o.ncols, o.pos[: rows + 1], o.idx[:e], o.vals[:e]))
+        return sub
+
+    def ref_run(self, sample, nthreads):
+        import oracle
+
+        out = oracle.ref_spadd(sample, nthreads)
+        return sum(_csr_bytes(o) for o in sample) + 8 * (out["nrows"] + 1) + 16 * int(
+            out["pos"][-1]), sum(o.nnz for o in sample[1:])
+
+    def total_rows(self):
+        return self.cfg["ops"][0].nrows
+
+
+WORKLOADS = {2: SpaddWork}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        return time.time()
+
+    def stop(self, t0, t1):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [l for (t, l) in self.lines if t0 - 0.06 <= t <= t1 + 0.06] or [
+            l for (_, l) in self.lines[-3:]]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in rows:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except Exception:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, cid):
+    """--impl reference: the reference CPU path alone, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    W = WORKLOADS[cid](cid, 0)
+    kind = "reference" if oracle.ref_available() else "port"
+    if kind != "reference":
+        raise SystemExit("oracle/_ref missing; run __graft_entry__.build() where /root/reference exists")
+    nthreads = os.cpu_count() or 1
+    rows = W.total_rows()
+    # size the per-step sample so the whole run ends within a few minutes
+    t = time.perf_counter()
+    W.ref_run(W.ref_sample(max(1, rows // 20)), nthreads)
+    est_full = (time.perf_counter() - t) * 20
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    if est_full > budget:
+        rows = max(1, int(rows * budget / est_full))
+    sample = W.ref_sample(rows)
+    for _ in range(args.warmup):
+        W.ref_run(sample, nthreads)
+    times, nbytes, flops = [], 0, 0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        nbytes, flops = W.ref_run(sample, nthreads)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    value = nbytes * args.steps / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": W.name, "config_id": cid, "sample_rows": rows,
+                   "total_rows": W.total_rows()},
+        "useful_gflops": flops * args.steps / tot / 1e9,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nthreads, "kind": kind,
+                         "sample": f"first {rows} of {W.total_rows()} rows per step, "
+                                   f"{nthreads} threads (row blocks, one Workspace each)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(W, target_s=10.0):
+    import oracle
+
+    kind = "reference" if oracle.ref_available() else "port"
+    nthreads = os.cpu_count() or 1
+    rows = W.total_rows()
+    sample = W.ref_sample(rows)
+    reps, t_all, nbytes = 0, 0.0, 0
+    rates = []
+    while (t_all < target_s and reps < 5) or reps < 2:
+        t = time.perf_counter()
+        if kind == "reference":
+            nbytes, _ = W.ref_run(sample, nthreads)
+        dt = time.perf_counter() - t
+        rates.append(nbytes / dt / 1e9)
+        t_all += dt
+        reps += 1
+    return {"value": statistics.median(rates), "unit": "GB/s", "cores": nthreads, "kind": kind,
+            "sample": f"full config, {reps} repetitions, median; reference Workspace/"
+                      f"TensorBuilder over {nthreads} host threads (row blocks)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cid = args.config
+    if cid not in WORKLOADS:
+        raise SystemExit(f"config {cid} not available in this build")
+    if args.impl == "reference":
+        return run_reference(args, cid)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1802_10574_b200 import Context
+
+    W = WORKLOADS[cid](cid, rank)
+    ctx = Context(local)
+    stream = torch.cuda.Stream(device=local)
+    ctx.set_stream(stream)
+    W.setup(ctx)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            W.step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.time()
+        ev0.record(stream)
+        launches = 0
+        for _ in range(args.steps):
+            st = W.step()
+            launches += st.kernel_launches
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    clk = clocks.stop(t0, t1)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    # kernel timings (separate pass with per-kernel events)
+    kms, tot_ms, kname = [], [], ""
+    with torch.cuda.stream(stream):
+        for _ in range(max(5, min(args.steps, 50))):
+            st = W.step(timing=True)
+            kms.append(st.main_kernel_ms)
+            tot_ms.append(st.total_kernel_ms)
+            kname = st.main_kernel.decode()
+    kernel_ms = statistics.mean(kms)
+    # e2e through the C ABI with pinned host buffers
+    e2e_times = []
+    for _ in range(max(3, min(args.steps, 10))):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        W.e2e_step()
+        e2e_times.append(time.perf_counter() - t)
+    e2e_s = statistics.median(e2e_times)
+
+    algo = W.algo_bytes()
+    per_rank = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(per_rank, op=dist.ReduceOp.MAX)
+    ms_max, e2e_max = per_rank.tolist()
+    value = algo * world / (ms_max * 1e-3) / 1e9
+    peak, peak_src = _peak_hbm()
+    achieved = algo / (kernel_ms * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded; BASELINE shapes, see DESIGN.md)",
+            "config": {"workload": W.name, "config_id": cid,
+                       "l2": "inputs larger than L2 (no flush)" if W.in_bytes > 126e6
+                       else "inputs smaller than L2",
+                       "algo_bytes_per_step": algo, "nnz_out": W.nnz_out,
+                       "parallelism": f"row shards x{world} (weak)"},
+            "useful_gflops": W.flops() * world / (ms_max * 1e-3) / 1e9,
+            "kernel_ms": kernel_ms, "kernels_total_ms": statistics.mean(tot_ms),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _traffic(W.name, kname),
+                         "kernel": kname, "peak_source": peak_src},
+            "e2e": {"value": algo * world / e2e_max / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": W.h2d_bytes(), "d2h_bytes_per_step": W.d2h_bytes(),
+                    "ms_per_step": e2e_max * 1e3},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(W)
+            except Exception as e:  # the baseline must not kill the GPU number
+                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

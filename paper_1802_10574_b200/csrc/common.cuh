@@ -1,0 +1,147 @@
+// common.cuh — shared device helpers for the sm_100a workspace kernels.
+//
+// Everything here is plain CUDA C++ for sm_100a: warp primitives
+// (shfl/ballot/match), an ordered-tile decoupled look-back used by the
+// single-pass kernels (SpAdd, sparse MTTKRP) to turn per-tile output counts
+// into output offsets without a separate symbolic pass, and a few math
+// helpers that pin the rounding of the reference's accumulations.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stamgpu {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// The reference accumulates `w += a*b` with the product rounded first
+// (Workspace::insert receives the already-rounded product,
+// workspace.cpp:34-46).  The oracle is compiled with -ffp-contract=off; these
+// helpers stop nvcc from contracting into an FMA so results stay bit-exact.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T u = __shfl_xor_sync(kFull, v, o);
+    v = u > v ? u : v;
+  }
+  return v;
+}
+
+// Inclusive warp prefix sum.
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(kFull, v, o);
+    if (lane >= (unsigned)o) v += u;
+  }
+  return v;
+}
+
+// Read-only streaming loads (bypass L1 allocation for data touched once).
+__device__ __forceinline__ int64_t ldg_stream(const int64_t* p) {
+  return (int64_t)__ldcs((const long long*)p);
+}
+__device__ __forceinline__ double ldg_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ void stg_stream(int64_t* p, int64_t v) {
+  __stcs((long long*)p, (long long)v);
+}
+__device__ __forceinline__ void stg_stream(double* p, double v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------------------
+// Ordered tiles with decoupled look-back.
+//
+// Tiles are claimed in increasing order through an atomic counter, so every
+// predecessor of a claimed tile is already running; a tile publishes its
+// aggregate, looks back over its predecessors' published values and publishes
+// its inclusive prefix.  Status word: bits 63..62 flag (0 none, 1 aggregate,
+// 2 inclusive prefix), bits 61..0 value.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagInc = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Called by one full warp of the tile.  Returns the exclusive prefix (sum of
+// all predecessors' aggregates) in every lane.
+__device__ __forceinline__ int64_t lookback_exclusive(uint64_t* status, int64_t tile,
+                                                      int64_t aggregate) {
+  const unsigned lane = lane_id();
+  if (tile == 0) {
+    if (lane == 0) st_release(&status[0], kFlagInc | (uint64_t)aggregate);
+    return 0;
+  }
+  if (lane == 0) st_release(&status[tile], kFlagAgg | (uint64_t)aggregate);
+  int64_t exclusive = 0;
+  int64_t base = tile - 1;  // window covers [base-31, base]
+  while (true) {
+    const int64_t t = base - (int64_t)lane;
+    uint64_t s = kFlagInc;  // lanes before tile 0 behave like a zero prefix
+    if (t >= 0) {
+      do {
+        s = ld_acquire(&status[t]);
+      } while ((s >> 62) == 0);
+    }
+    const unsigned inc_mask = __ballot_sync(kFull, (s >> 62) == 2);
+    // closest predecessor holding an inclusive prefix = lowest set lane
+    const int stop = inc_mask ? __ffs(inc_mask) - 1 : 32;
+    int64_t v = (lane <= (unsigned)stop && t >= 0) ? (int64_t)(s & kValMask) : 0;
+    exclusive += warp_sum(v);
+    if (inc_mask) break;
+    base -= 32;
+  }
+  if (lane == 0) st_release(&status[tile], kFlagInc | (uint64_t)(exclusive + aggregate));
+  return exclusive;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x multiple of 32,
+// <= 1024).  `sh` needs 33 ints.  Returns exclusive prefix, total in *total.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* sh, int* total) {
+  const unsigned lane = lane_id();
+  const unsigned warp = threadIdx.x >> 5;
+  const unsigned nwarps = blockDim.x >> 5;
+  int inc = warp_inclusive_scan(v);
+  if (lane == 31) sh[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nwarps ? sh[lane] : 0;
+    int winc = warp_inclusive_scan(w);
+    if (lane < nwarps) sh[lane] = winc - w;
+    if (lane == nwarps - 1) sh[32] = winc;
+  }
+  __syncthreads();
+  int res = inc - v + sh[warp];
+  if (total) *total = sh[32];
+  __syncthreads();
+  return res;
+}
+
+}  // namespace stamgpu

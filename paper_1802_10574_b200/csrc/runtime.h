@@ -1,0 +1,152 @@
+// runtime.h — host-side runtime shared by the kernel translation units:
+// the context (device, stream, stream-ordered pool, pinned result cache,
+// timing events), per-call scratch scopes, input staging, and the error
+// convention of the C ABI (stam_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "stam_cuda.h"
+
+namespace stamrt {
+
+// Internal failure; converted to a status code at the C ABI boundary.
+struct Failure {
+  int code;
+  std::string message;
+};
+
+[[noreturn]] void fail(int code, const std::string& message);
+void set_last_error(const std::string& message);
+
+#define STAM_CUDA_CHECK(expr)                                                   \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::stamrt::fail(_e == cudaErrorMemoryAllocation ? STAM_ERR_OUT_OF_MEMORY   \
+                                                     : STAM_ERR_CUDA,           \
+                     std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+    }                                                                           \
+  } while (0)
+
+struct TimedLaunch {
+  const char* name;
+  cudaEvent_t start, stop;
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  // pinned host memory returned by released host results, reused by size
+  std::vector<std::pair<void*, size_t>> pinned_free;
+  // small pinned scalars for count read-back
+  int64_t* h_scalars = nullptr;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+};
+
+// Result ownership record behind stam_*_result.handle.
+struct Owned {
+  void* dev = nullptr;
+  void* host = nullptr;
+  size_t host_bytes = 0;
+};
+
+// Per-call state: temporary device allocations (freed stream-ordered at the
+// end of the call), timing events and launch counts.
+class Call {
+ public:
+  Call(Ctx* ctx, const stam_options* opts, stam_stats* stats);
+  ~Call();
+
+  Ctx* ctx() const { return ctx_; }
+  cudaStream_t stream() const { return ctx_->stream; }
+  const stam_options& opts() const { return opts_; }
+
+  // Temporary device allocation released when the call ends.
+  void* scratch(size_t bytes);
+  template <typename T>
+  T* scratch_n(size_t n) {
+    return static_cast<T*>(scratch(n * sizeof(T)));
+  }
+  // Zero-filled temporary allocation.
+  void* scratch_zero(size_t bytes);
+
+  // Device pointer for a possibly-host input array (copied H2D when needed).
+  template <typename T>
+  const T* device_input(const T* p, size_t n, int32_t mem) {
+    return static_cast<const T*>(stage(p, n * sizeof(T), mem));
+  }
+
+  // Launch bookkeeping: call before/after each kernel launch.
+  void before_launch(const char* name);
+  void after_launch();
+
+  // Read one int64 from device memory (synchronizes the stream).
+  int64_t read_scalar(const int64_t* dptr);
+  void read_scalars(const int64_t* dptr, int n, int64_t* out);
+
+  // Result buffers: one device block holding pos/idx/vals (or vals only).
+  void alloc_csr_result(stam_csr_result* r, int64_t nrows, int64_t ncols, int64_t nnz_capacity);
+  void finish_csr_result(stam_csr_result* r, int64_t nnz);
+  void alloc_dense_result(stam_dense_result* r, int64_t nrows, int64_t ncols);
+  void finish_dense_result(stam_dense_result* r);
+
+  // Synchronize, harvest timings into stats.
+  void finish();
+
+  stam_stats* stats() { return stats_; }
+
+ private:
+  const void* stage(const void* p, size_t bytes, int32_t mem);
+  void* pinned_alloc(size_t bytes);
+
+  Ctx* ctx_;
+  stam_options opts_;
+  stam_stats* stats_;
+  stam_stats local_stats_;
+  std::vector<void*> temps_;
+  std::vector<TimedLaunch> launches_;
+  cudaEvent_t h2d_start_ = nullptr, h2d_stop_ = nullptr;
+  cudaEvent_t d2h_start_ = nullptr, d2h_stop_ = nullptr;
+  bool finished_ = false;
+  int pending_ = -1;
+};
+
+// Runs `fn` translating Failure / std::exception into status codes.
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return STAM_OK;
+  } catch (const Failure& f) {
+    set_last_error(f.message);
+    return f.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return STAM_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return STAM_ERR_INTERNAL;
+  }
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Validates a CSR view's scalar fields (array contents are trusted; the C++
+// wrapper validates storage before calling, as TensorStorage::validate does).
+void check_csr_view(const stam_csr_view* v, const char* what);
+void check_csf3_view(const stam_csf3_view* v, const char* what);
+void check_dense_view(const stam_dense_view* v, const char* what);
+
+}  // namespace stamrt

@@ -1,0 +1,542 @@
+// spadd.cu — multi-operand SpAdd  D = ops[0] + ops[1] + ... (CSR, sorted).
+//
+// Reference semantics: one row workspace per output row, the
+// first operand assigned and the others accumulated in operand order, then a
+// sorted drain (golden CIN test_transform.cpp:275-284; Workspace::insert
+// workspace.cpp:34-46; drain workspace.cpp:62-71).  No pairwise merge.
+//
+// B200 design:
+//  * one kernel, one pass over the inputs: ordered tiles of 16 rows claimed
+//    through an atomic counter; every tile merges its rows in shared memory,
+//    publishes its output count and learns its output offset by decoupled
+//    look-back, then streams its staged rows out.  Inputs are read once and the
+//    output written once, the HBM minimum.
+//  * the row workspace is a rank-merge in shared memory: each stored element
+//    finds its position in the operand-ordered merge by binary search into the
+//    other operands' rows (already staged in smem), so the row is "scattered"
+//    into its sorted slot; equal columns land adjacent in operand order and are
+//    combined exactly as the workspace would (w = a; w += b; w += c ...), so
+//    values are bit-identical to the CPU reference.
+//  * rows too long for a warp's staging go to a CTA-per-row kernel with a
+//    windowed column bitmap (also operand-ordered, also bit-exact).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "common.cuh"
+#include "runtime.h"
+
+namespace stamgpu {
+namespace {
+
+constexpr int kMaxOps = 16;
+constexpr int kWarps = 8;
+constexpr int kRowsPerWarp = 2;
+constexpr int kTileRows = kWarps * kRowsPerWarp;
+constexpr int kStage = 384;  // staged entries per warp
+
+enum RowState : int { kStaged = 0, kPostponed = 1, kDeferred = 2 };
+
+struct SpaddParams {
+  const int64_t* pos[kMaxOps];
+  const int64_t* idx[kMaxOps];
+  const double* vals[kMaxOps];
+  int nops;
+  int64_t nrows;
+  int64_t ntiles;
+  int64_t* out_pos;
+  int64_t* out_idx;
+  double* out_vals;
+  uint64_t* tile_status;
+  unsigned long long* tile_counter;
+  int64_t* deferred_rows;
+  unsigned long long* deferred_count;
+  int64_t* total_nnz;
+};
+
+template <typename ColT>
+struct WarpStage {
+  ColT in_col[kStage];
+  ColT st_col[kStage];
+  double st_val[kStage];
+  uint8_t st_op[kStage];
+  // current row's operand segments
+  int64_t seg_beg[kMaxOps];
+  int seg_len[kMaxOps];
+  int seg_co[kMaxOps];
+};
+
+template <typename ColT>
+struct TileSmem {
+  WarpStage<ColT> w[kWarps];
+  int64_t tpos[kMaxOps][kTileRows + 1];
+  int64_t row_cnt[kTileRows];
+  int64_t row_dst[kTileRows];
+  int row_state[kTileRows];
+  int row_off[kTileRows];
+  int64_t tile_id;
+};
+
+// Number of elements < x (lower) or <= x (upper) in sorted s[0..n).
+template <typename ColT>
+__device__ __forceinline__ int rank_lower(const ColT* s, int n, ColT x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (s[lo + h] < x) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo;
+}
+template <typename ColT>
+__device__ __forceinline__ int rank_upper(const ColT* s, int n, ColT x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (s[lo + h] <= x) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t lower_bound_global(const int64_t* s, int64_t n, int64_t x) {
+  int64_t lo = 0;
+  while (n > 0) {
+    const int64_t h = n >> 1;
+    if (__ldg(s + lo + h) < x) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo;
+}
+
+// Fill the warp's segment table for tile row r; returns the exact total.
+template <typename ColT>
+__device__ __forceinline__ int64_t row_segments(const TileSmem<ColT>& S, WarpStage<ColT>& W,
+                                                int nops, int r) {
+  const unsigned lane = lane_id();
+  int64_t b = 0, e = 0;
+  if ((int)lane < nops) {
+    b = S.tpos[lane][r];
+    e = S.tpos[lane][r + 1];
+  }
+  const int64_t len = e - b;
+  const int64_t inc = warp_inclusive_scan(len);
+  const int64_t tot = __shfl_sync(kFull, inc, 31);
+  if ((int)lane < nops) {
+    W.seg_beg[lane] = b;
+    // only trusted when tot fits the staging buffer
+    W.seg_len[lane] = (int)min(len, (int64_t)0x3fffffff);
+    W.seg_co[lane] = (int)min(inc - len, (int64_t)0x3fffffff);
+  }
+  __syncwarp();
+  return tot;
+}
+
+// Stage the row's column segments, concatenated in operand order, into in_col.
+template <typename ColT>
+__device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT>& W) {
+  const unsigned lane = lane_id();
+  for (int p = 0; p < P.nops; p++) {
+    const int64_t* src = P.idx[p] + W.seg_beg[p];
+    const int len = W.seg_len[p];
+    ColT* dst = W.in_col + W.seg_co[p];
+    for (int t = lane; t < len; t += 32) dst[t] = (ColT)ldg_stream(src + t);
+  }
+  __syncwarp();
+}
+
+// Rank-merge the staged row into st_* at [out, out+L) (operand order on ties),
+// then combine equal columns in place.  Returns the number of distinct columns.
+template <typename ColT>
+__device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int out) {
+  const unsigned lane = lane_id();
+  const int nops = P.nops;
+  ColT* st_col = W.st_col + out;
+  double* st_val = W.st_val + out;
+  uint8_t* st_op = W.st_op + out;
+  // scatter every element to its merged slot
+  for (int o = 0; o < nops; o++) {
+    const double* vsrc = P.vals[o] + W.seg_beg[o];
+    const int len = W.seg_len[o];
+    const int co = W.seg_co[o];
+    for (int t = lane; t < len; t += 32) {
+      const double v = ldg_stream(vsrc + t);
+      const ColT x = W.in_col[co + t];
+      int m = t;
+      for (int q = 0; q < nops; q++) {
+        if (q == o) continue;
+        const ColT* sq = W.in_col + W.seg_co[q];
+        const int nq = W.seg_len[q];
+        m += (q < o) ? rank_upper(sq, nq, x) : rank_lower(sq, nq, x);
+      }
+      st_col[m] = x;
+      st_val[m] = v;
+      st_op[m] = (uint8_t)o;
+    }
+  }
+  __syncwarp();
+  // combine runs of equal columns in operand order; compact in place
+  int count = 0;
+  ColT prev = 0;
+  for (int base = 0; base < L; base += 32) {
+    const int m = base + (int)lane;
+    ColT x = 0;
+    double w = 0.0;
+    bool lead = false;
+    if (m < L) {
+      x = st_col[m];
+      const ColT before = (lane == 0) ? prev : st_col[m - 1];
+      lead = (m == 0) || (before != x);
+      if (lead) {
+        const double v0 = st_val[m];
+        w = (st_op[m] == 0) ? v0 : add_rn(0.0, v0);  // assign vs accumulate into 0.0
+        for (int n = m + 1; n < L && st_col[n] == x; n++) w = add_rn(w, st_val[n]);
+      }
+    }
+    prev = __shfl_sync(kFull, x, 31);
+    const unsigned lead_mask = __ballot_sync(kFull, lead);
+    const int slot = count + __popc(lead_mask & lanemask_lt());
+    __syncwarp();
+    if (lead) {
+      st_col[slot] = x;
+      st_val[slot] = w;
+    }
+    __syncwarp();
+    count += __popc(lead_mask);
+  }
+  return count;
+}
+
+// Distinct-column count of a staged row (in_col only, no merge written).
+template <typename ColT>
+__device__ int count_row(const SpaddParams& P, const WarpStage<ColT>& W) {
+  const unsigned lane = lane_id();
+  int count = W.seg_len[0];  // every first-operand entry starts a column
+  for (int o = 1; o < P.nops; o++) {
+    const int len = W.seg_len[o];
+    const int co = W.seg_co[o];
+    for (int t0 = 0; t0 < len; t0 += 32) {
+      const int t = t0 + (int)lane;
+      bool lead = false;
+      if (t < len) {
+        const ColT x = W.in_col[co + t];
+        lead = true;
+        for (int q = 0; q < o && lead; q++) {
+          const ColT* sq = W.in_col + W.seg_co[q];
+          const int nq = W.seg_len[q];
+          const int r = rank_lower(sq, nq, x);
+          if (r < nq && sq[r] == x) lead = false;
+        }
+      }
+      count += __popc(__ballot_sync(kFull, lead));
+    }
+  }
+  return count;
+}
+
+// Distinct-column count of a row read straight from global memory (rows that
+// exceed the staging buffer; their values are written by the long-row kernel).
+template <typename ColT>
+__device__ int64_t count_row_global(const SpaddParams& P, const TileSmem<ColT>& S, int r) {
+  const unsigned lane = lane_id();
+  int64_t count = S.tpos[0][r + 1] - S.tpos[0][r];
+  for (int o = 1; o < P.nops; o++) {
+    const int64_t bo = S.tpos[o][r], lo = S.tpos[o][r + 1] - bo;
+    for (int64_t t0 = 0; t0 < lo; t0 += 32) {
+      const int64_t t = t0 + lane;
+      bool lead = false;
+      if (t < lo) {
+        const int64_t x = __ldg(P.idx[o] + bo + t);
+        lead = true;
+        for (int q = 0; q < o && lead; q++) {
+          const int64_t bq = S.tpos[q][r], lq = S.tpos[q][r + 1] - bq;
+          const int64_t k = lower_bound_global(P.idx[q] + bq, lq, x);
+          if (k < lq && __ldg(P.idx[q] + bq + k) == x) lead = false;
+        }
+      }
+      count += __popc(__ballot_sync(kFull, lead));
+    }
+  }
+  return count;
+}
+
+template <typename ColT>
+__global__ void __launch_bounds__(kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem<ColT>& S = *reinterpret_cast<TileSmem<ColT>*>(smem_raw);
+  const unsigned lane = lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int nops = P.nops;
+
+  if (threadIdx.x == 0) S.tile_id = (int64_t)atomicAdd(P.tile_counter, 1ull);
+  __syncthreads();
+  const int64_t tile = S.tile_id;
+  const int64_t row0 = tile * kTileRows;
+  const int nrows_tile = (int)min((int64_t)kTileRows, P.nrows - row0);
+
+  // tile-wide operand row pointers
+  for (int i = threadIdx.x; i < nops * (kTileRows + 1); i += blockDim.x) {
+    const int p = i / (kTileRows + 1);
+    const int r = i % (kTileRows + 1);
+    S.tpos[p][r] = (r <= nrows_tile) ? __ldg(P.pos[p] + row0 + r) : 0;
+  }
+  __syncthreads();
+
+  WarpStage<ColT>& W = S.w[warp];
+  int stage_off = 0;
+  for (int k = 0; k < kRowsPerWarp; k++) {
+    const int r = warp * kRowsPerWarp + k;
+    if (r >= nrows_tile) break;
+    const int64_t tot = row_segments(S, W, nops, r);
+    int64_t cnt;
+    int state;
+    if (tot <= kStage - stage_off) {
+      load_cols(P, W);
+      cnt = merge_row(P, W, (int)tot, stage_off);
+      state = kStaged;
+    } else if (tot <= kStage) {
+      load_cols(P, W);
+      cnt = count_row(P, W);
+      state = kPostponed;
+    } else {
+      cnt = count_row_global(P, S, r);
+      state = kDeferred;
+    }
+    if (lane == 0) {
+      S.row_cnt[r] = cnt;
+      S.row_state[r] = state;
+      S.row_off[r] = stage_off;
+    }
+    if (state == kStaged) stage_off += (int)cnt;
+    __syncwarp();
+  }
+  __syncthreads();
+
+  // tile aggregate and look-back (warp 0)
+  if (warp == 0) {
+    const int64_t c = (int)lane < nrows_tile ? S.row_cnt[lane] : 0;
+    const int64_t inc = warp_inclusive_scan(c);
+    const int64_t agg = __shfl_sync(kFull, inc, 31);
+    const int64_t base = lookback_exclusive(P.tile_status, tile, agg);
+    if ((int)lane < nrows_tile) {
+      S.row_dst[lane] = base + inc - c;
+      P.out_pos[row0 + lane + 1] = base + inc;
+    }
+    if (lane == 0) {
+      if (tile == 0) P.out_pos[0] = 0;
+      if (tile == P.ntiles - 1) *P.total_nnz = base + agg;
+    }
+  }
+  __syncthreads();
+
+  // stream out staged rows; redo postponed rows with the (now free) staging
+  for (int k = 0; k < kRowsPerWarp; k++) {
+    const int r = warp * kRowsPerWarp + k;
+    if (r >= nrows_tile) break;
+    if (S.row_state[r] != kStaged) continue;
+    const int64_t dst = S.row_dst[r];
+    const int off = S.row_off[r];
+    const int cnt = (int)S.row_cnt[r];
+    for (int t = lane; t < cnt; t += 32) {
+      stg_stream(P.out_idx + dst + t, (int64_t)W.st_col[off + t]);
+      stg_stream(P.out_vals + dst + t, W.st_val[off + t]);
+    }
+  }
+  __syncwarp();
+  for (int k = 0; k < kRowsPerWarp; k++) {
+    const int r = warp * kRowsPerWarp + k;
+    if (r >= nrows_tile) break;
+    const int state = S.row_state[r];
+    if (state == kPostponed) {
+      const int64_t dst = S.row_dst[r];
+      const int64_t tot = row_segments(S, W, nops, r);
+      load_cols(P, W);
+      const int cnt = merge_row(P, W, (int)tot, 0);
+      for (int t = lane; t < cnt; t += 32) {
+        stg_stream(P.out_idx + dst + t, (int64_t)W.st_col[t]);
+        stg_stream(P.out_vals + dst + t, W.st_val[t]);
+      }
+      __syncwarp();
+    } else if (state == kDeferred && lane == 0) {
+      const unsigned long long slot = atomicAdd(P.deferred_count, 1ull);
+      P.deferred_rows[slot] = row0 + r;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Long rows: one CTA per row, windowed column bitmap.  For each window of
+// kWinBits columns the CTA marks present columns, ranks them by popcount
+// prefix, zeroes the window's output slots and then applies the operands in
+// order (assign, then accumulate) — the workspace semantics, bit-exact.
+// ---------------------------------------------------------------------------
+constexpr int kLongThreads = 512;
+constexpr int kWinWords = 2048;
+constexpr int64_t kWinBits = (int64_t)kWinWords * 32;
+
+__global__ void __launch_bounds__(kLongThreads) spadd_long_rows_kernel(const SpaddParams P) {
+  __shared__ uint32_t bits[kWinWords];
+  __shared__ int wpre[kWinWords];
+  __shared__ int64_t head[kMaxOps], stop[kMaxOps], wend[kMaxOps];
+  __shared__ int64_t c0_sh;
+  __shared__ int scan_sh[33];
+  const int tid = threadIdx.x;
+  const int nops = P.nops;
+  const unsigned long long ndef = *P.deferred_count;
+  for (unsigned long long d = blockIdx.x; d < ndef; d += gridDim.x) {
+    const int64_t r = P.deferred_rows[d];
+    if (tid < nops) {
+      head[tid] = __ldg(P.pos[tid] + r);
+      stop[tid] = __ldg(P.pos[tid] + r + 1);
+    }
+    for (int w = tid; w < kWinWords; w += blockDim.x) bits[w] = 0u;
+    int64_t dst = P.out_pos[r];
+    __syncthreads();
+    while (true) {
+      if (tid == 0) {
+        int64_t c0 = INT64_MAX;
+        for (int p = 0; p < nops; p++)
+          if (head[p] < stop[p]) c0 = min(c0, __ldg(P.idx[p] + head[p]));
+        c0_sh = c0;
+      }
+      __syncthreads();
+      const int64_t c0 = c0_sh;
+      if (c0 == INT64_MAX) break;
+      if (tid < nops) {
+        wend[tid] = head[tid] +
+                    lower_bound_global(P.idx[tid] + head[tid], stop[tid] - head[tid], c0 + kWinBits);
+      }
+      __syncthreads();
+      for (int p = 0; p < nops; p++) {
+        for (int64_t t = head[p] + tid; t < wend[p]; t += blockDim.x) {
+          const int64_t c = __ldg(P.idx[p] + t) - c0;
+          atomicOr(&bits[c >> 5], 1u << (c & 31));
+        }
+      }
+      __syncthreads();
+      // exclusive popcount prefix over the window's words
+      constexpr int kPer = kWinWords / kLongThreads;
+      int local[kPer];
+      int sum = 0;
+#pragma unroll
+      for (int q = 0; q < kPer; q++) {
+        local[q] = sum;
+        sum += __popc(bits[tid * kPer + q]);
+      }
+      int total;
+      const int base = block_exclusive_scan(sum, scan_sh, &total);
+#pragma unroll
+      for (int q = 0; q < kPer; q++) wpre[tid * kPer + q] = base + local[q];
+      for (int t = tid; t < total; t += blockDim.x) P.out_vals[dst + t] = 0.0;
+      __syncthreads();
+      for (int p = 0; p < nops; p++) {
+        for (int64_t t = head[p] + tid; t < wend[p]; t += blockDim.x) {
+          const int64_t col = __ldg(P.idx[p] + t);
+          const int64_t c = col - c0;
+          const int w = (int)(c >> 5);
+          const int rank = wpre[w] + __popc(bits[w] & ((1u << (c & 31)) - 1u));
+          const double v = __ldg(P.vals[p] + t);
+          P.out_idx[dst + rank] = col;
+          P.out_vals[dst + rank] = (p == 0) ? v : add_rn(P.out_vals[dst + rank], v);
+        }
+        __syncthreads();
+      }
+      for (int w = tid; w < kWinWords; w += blockDim.x) bits[w] = 0u;
+      if (tid < nops) head[tid] = wend[tid];
+      dst += total;
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+}
+
+template <typename ColT>
+void launch_tiles(stamrt::Call& call, const SpaddParams& P) {
+  const size_t smem = sizeof(TileSmem<ColT>);
+  auto kern = spadd_tiles_kernel<ColT>;
+  STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  call.before_launch(sizeof(ColT) == 4 ? "spadd_tiles<u32>" : "spadd_tiles<i64>");
+  kern<<<(unsigned)P.ntiles, kWarps * 32, smem, call.stream()>>>(P);
+  call.after_launch();
+}
+
+}  // namespace
+}  // namespace stamgpu
+
+using namespace stamrt;
+
+extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,
+                               const stam_options* opts, stam_csr_result* D, stam_stats* stats) {
+  using namespace stamgpu;
+  return guarded([&] {
+    Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
+    if (!ops) fail(STAM_ERR_PRECONDITION_VIOLATED, "null operand array");
+    if (nops < 2) fail(STAM_ERR_ARITY_MISMATCH, "spadd needs at least two operands");
+    if (nops > kMaxOps)
+      fail(STAM_ERR_UNSUPPORTED_MERGE, "spadd supports at most 16 operands per call");
+    for (int p = 0; p < nops; p++) {
+      check_csr_view(&ops[p], "spadd operand");
+      if (ops[p].nrows != ops[0].nrows || ops[p].ncols != ops[0].ncols)
+        fail(STAM_ERR_DIMENSION_MISMATCH, "spadd operands must have equal dimensions");
+    }
+    if (call.opts().mode != STAM_MODE_FUSED)
+      fail(STAM_ERR_UNSUPPORTED_MERGE, "spadd supports fused mode only in ABI v1");
+    const int64_t nrows = ops[0].nrows, ncols = ops[0].ncols;
+    SpaddParams P{};
+    P.nops = nops;
+    P.nrows = nrows;
+    int64_t cap = 0, accum = 0;
+    for (int p = 0; p < nops; p++) {
+      P.pos[p] = call.device_input(ops[p].pos, (size_t)nrows + 1, ops[p].mem);
+      P.idx[p] = call.device_input(ops[p].idx, (size_t)ops[p].nnz, ops[p].mem);
+      P.vals[p] = call.device_input(ops[p].vals, (size_t)ops[p].nnz, ops[p].mem);
+      cap += ops[p].nnz;
+      if (p > 0) accum += ops[p].nnz;
+    }
+    P.ntiles = ceil_div(nrows, kTileRows);
+    call.alloc_csr_result(D, nrows, ncols, cap);
+    P.out_pos = D->pos;
+    P.out_idx = D->idx;
+    P.out_vals = D->vals;
+    // control block: [tile counter, deferred count, total] + tile status words
+    const size_t ctl_words = 4 + (size_t)P.ntiles;
+    auto* ctl = static_cast<uint64_t*>(call.scratch_zero(ctl_words * sizeof(uint64_t)));
+    P.tile_counter = reinterpret_cast<unsigned long long*>(ctl);
+    P.deferred_count = reinterpret_cast<unsigned long long*>(ctl + 1);
+    P.total_nnz = reinterpret_cast<int64_t*>(ctl + 2);
+    P.tile_status = ctl + 4;
+    const int64_t max_deferred = std::min<int64_t>(nrows, cap / kStage + 1);
+    P.deferred_rows = call.scratch_n<int64_t>((size_t)max_deferred);
+
+    if (ncols <= (int64_t)UINT32_MAX)
+      launch_tiles<uint32_t>(call, P);
+    else
+      launch_tiles<int64_t>(call, P);
+    call.before_launch("spadd_long_rows");
+    spadd_long_rows_kernel<<<(unsigned)std::max(1, call.ctx()->num_sms), kLongThreads, 0,
+                             call.stream()>>>(P);
+    call.after_launch();
+
+    const int64_t nnz = call.read_scalar(P.total_nnz);
+    call.finish_csr_result(D, nnz);
+    call.finish();
+    stam_stats* st = call.stats();
+    st->adds = accum;
+    st->ws_inserts = cap;
+    st->ws_resets = nrows;
+    st->appends = nnz;
+  });
+}
