@@ -79,33 +79,25 @@ struct TileSmem {
 };
 
 // Number of elements < x (lower) or <= x (upper) in sorted s[0..n).
+// Branchless; trip count = bit length of n, uniform across a warp searching
+// one operand row.
 template <typename ColT>
 __device__ __forceinline__ int rank_lower(const ColT* s, int n, ColT x) {
-  int lo = 0;
-  while (n > 0) {
-    const int h = n >> 1;
-    if (s[lo + h] < x) {
-      lo += h + 1;
-      n -= h + 1;
-    } else {
-      n = h;
-    }
+  int pos = 0;
+  for (int step = n ? (1 << (31 - __clz(n))) : 0; step > 0; step >>= 1) {
+    const int probe = pos + step;
+    pos = (probe <= n && s[probe - 1] < x) ? probe : pos;
   }
-  return lo;
+  return pos;
 }
 template <typename ColT>
 __device__ __forceinline__ int rank_upper(const ColT* s, int n, ColT x) {
-  int lo = 0;
-  while (n > 0) {
-    const int h = n >> 1;
-    if (s[lo + h] <= x) {
-      lo += h + 1;
-      n -= h + 1;
-    } else {
-      n = h;
-    }
+  int pos = 0;
+  for (int step = n ? (1 << (31 - __clz(n))) : 0; step > 0; step >>= 1) {
+    const int probe = pos + step;
+    pos = (probe <= n && s[probe - 1] <= x) ? probe : pos;
   }
-  return lo;
+  return pos;
 }
 
 __device__ __forceinline__ int64_t lower_bound_global(const int64_t* s, int64_t n, int64_t x) {
@@ -168,6 +160,7 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int ou
   double* st_val = W.st_val + out;
   uint8_t* st_op = W.st_op + out;
   // scatter every element to its merged slot
+  bool dup = false;
   for (int o = 0; o < nops; o++) {
     const double* vsrc = P.vals[o] + W.seg_beg[o];
     const int len = W.seg_len[o];
@@ -180,7 +173,13 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int ou
         if (q == o) continue;
         const ColT* sq = W.in_col + W.seg_co[q];
         const int nq = W.seg_len[q];
-        m += (q < o) ? rank_upper(sq, nq, x) : rank_lower(sq, nq, x);
+        if (q < o) {
+          const int r = rank_upper(sq, nq, x);
+          dup |= r > 0 && sq[r - 1] == x;
+          m += r;
+        } else {
+          m += rank_lower(sq, nq, x);
+        }
       }
       st_col[m] = x;
       st_val[m] = v;
@@ -188,6 +187,8 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int ou
     }
   }
   __syncwarp();
+  // no column in two operands: the merge is already the compact row
+  if (!__any_sync(kFull, dup)) return L;
   // combine runs of equal columns in operand order; compact in place
   int count = 0;
   ColT prev = 0;
