@@ -37,6 +37,8 @@ import threading
 import time
 from pathlib import Path
 
+import numpy as np
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -175,7 +177,80 @@ class SpaddWork(Workload):
         return self.cfg["ops"][0].nrows
 
 
-WORKLOADS = {2: SpaddWork}
+class SpgemmWork(Workload):
+    """C = A*B (configs 1 and 3; config 3 squares A, so B is A)."""
+
+    def setup(self, ctx):
+        from paper_1802_10574_b200 import _native as N
+        from paper_1802_10574_b200.storage import CSR
+        import torch
+
+        self.N, self.ctx, self.lib = N, ctx, N.load()
+        A, B = self.cfg["A"], self.cfg["B"]
+        self.same = B is A
+        self.Ad = A.to("cuda")
+        self.Bd = self.Ad if self.same else B.to("cuda")
+        self.va, self.vb = self.Ad.view(), self.Bd.view()
+        pin = lambda m: CSR(m.nrows, m.ncols, *[torch.from_numpy(a).pin_memory()
+                                                for a in (m.pos, m.idx, m.vals)])
+        self.Ah = pin(A)
+        self.Bh = self.Ah if self.same else pin(B)
+        self.ha, self.hb = self.Ah.view(), self.Bh.view()
+        self.in_bytes = _csr_bytes(A) + (0 if self.same else _csr_bytes(B))
+        self.products = int(np.sum(np.diff(B.pos)[A.idx]))
+        self.nnz_out = None
+
+    def _call(self, va, vb, result_mem, timing):
+        N = self.N
+        r = N.CsrResult()
+        st = N.Stats()
+        opts = N.Options(1, 0, result_mem, 1 if timing else 0)
+        N.check(self.lib.stam_cuda_spgemm(self.ctx._ctx, C.byref(va), C.byref(vb), C.byref(opts),
+                                          C.byref(r), C.byref(st)))
+        self.nnz_out = r.nnz
+        self.out_bytes = 8 * (r.nrows + 1) + 16 * r.nnz
+        N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
+        return st
+
+    def step(self, timing=False):
+        return self._call(self.va, self.vb, self.N.STAM_MEM_DEVICE, timing)
+
+    def e2e_step(self):
+        return self._call(self.ha, self.hb, self.N.STAM_MEM_HOST, False)
+
+    def algo_bytes(self):
+        return self.in_bytes + self.out_bytes
+
+    def flops(self):
+        return 2 * self.products
+
+    def h2d_bytes(self):
+        return self.in_bytes
+
+    def d2h_bytes(self):
+        return self.out_bytes
+
+    def ref_sample(self, rows):
+        from paper_1802_10574_b200.storage import CSR
+
+        A = self.cfg["A"]
+        e = int(A.pos[rows])
+        return (CSR(rows, A.ncols, A.pos[: rows + 1], A.idx[:e], A.vals[:e]), self.cfg["B"])
+
+    def ref_run(self, sample, nthreads):
+        import oracle
+
+        A, B = sample
+        out = oracle.ref_spgemm(A, B, nthreads)
+        nbytes = _csr_bytes(A) + (0 if self.same else _csr_bytes(B)) + 8 * (out["nrows"] + 1) + \
+            16 * int(out["pos"][-1])
+        return nbytes, 2 * int(np.sum(np.diff(B.pos)[A.idx]))
+
+    def total_rows(self):
+        return self.cfg["A"].nrows
+
+
+WORKLOADS = {1: SpgemmWork, 2: SpaddWork, 3: SpgemmWork}
 
 
 # ---------------------------------------------------------------------------
