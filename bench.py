@@ -250,7 +250,104 @@ class SpgemmWork(Workload):
         return self.cfg["A"].nrows
 
 
-WORKLOADS = {1: SpgemmWork, 2: SpaddWork, 3: SpgemmWork}
+class MttkrpWork(Workload):
+    """A = B x_2 C x_3 D: dense factors (config 4) or CSR factors (config 5)."""
+
+    def setup(self, ctx):
+        from paper_1802_10574_b200 import _native as N
+        from paper_1802_10574_b200.storage import CSF3, CSR, Dense
+        import torch
+
+        self.N, self.ctx, self.lib = N, ctx, N.load()
+        B, Cf, Df = self.cfg["B"], self.cfg["C"], self.cfg["D"]
+        self.dense = isinstance(Cf, Dense)
+        self.Bd, self.Cd, self.Dd = B.to("cuda"), Cf.to("cuda"), Df.to("cuda")
+        self.vB, self.vC, self.vD = self.Bd.view(), self.Cd.view(), self.Dd.view()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        self.Bh = CSF3(B.dims, *[pin(a) for a in (B.pos1, B.idx1, B.pos2, B.idx2, B.vals)])
+        if self.dense:
+            self.Ch, self.Dh = Dense(pin(Cf.vals)), Dense(pin(Df.vals))
+            self.in_bytes = _csf_bytes(B) + 8 * (Cf.vals.size + Df.vals.size)
+            self.R = Cf.ncols
+            self.useful = 2 * self.R * (B.nnz + B.nfibers)
+        else:
+            self.Ch = CSR(Cf.nrows, Cf.ncols, *[pin(a) for a in (Cf.pos, Cf.idx, Cf.vals)])
+            self.Dh = CSR(Df.nrows, Df.ncols, *[pin(a) for a in (Df.pos, Df.idx, Df.vals)])
+            self.in_bytes = _csf_bytes(B) + _csr_bytes(Cf) + _csr_bytes(Df)
+            self.R = Cf.ncols
+            self.useful = None
+        self.hB, self.hC, self.hD = self.Bh.view(), self.Ch.view(), self.Dh.view()
+        self.nnz_out = None
+
+    def _call(self, vB, vC, vD, result_mem, timing):
+        N = self.N
+        st = N.Stats()
+        opts = N.Options(1, 0, result_mem, 1 if timing else 0)
+        if self.dense:
+            r = N.DenseResult()
+            N.check(self.lib.stam_cuda_mttkrp_dense(self.ctx._ctx, C.byref(vB), C.byref(vC),
+                                                    C.byref(vD), C.byref(opts), C.byref(r),
+                                                    C.byref(st)))
+            self.out_bytes = 8 * r.nrows * r.ncols
+            self.nnz_out = r.nrows * r.ncols
+        else:
+            r = N.CsrResult()
+            N.check(self.lib.stam_cuda_mttkrp_sparse(self.ctx._ctx, C.byref(vB), C.byref(vC),
+                                                     C.byref(vD), C.byref(opts), C.byref(r),
+                                                     C.byref(st)))
+            self.out_bytes = 8 * (r.nrows + 1) + 16 * r.nnz
+            self.nnz_out = r.nnz
+        N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
+        return st
+
+    def step(self, timing=False):
+        return self._call(self.vB, self.vC, self.vD, self.N.STAM_MEM_DEVICE, timing)
+
+    def e2e_step(self):
+        return self._call(self.hB, self.hC, self.hD, self.N.STAM_MEM_HOST, False)
+
+    def algo_bytes(self):
+        return self.in_bytes + self.out_bytes
+
+    def flops(self):
+        if self.useful is not None:
+            return self.useful
+        return 2 * (self._sparse_mults if hasattr(self, "_sparse_mults") else 0)
+
+    def h2d_bytes(self):
+        return self.in_bytes
+
+    def d2h_bytes(self):
+        return self.out_bytes
+
+    def ref_sample(self, slices):
+        from paper_1802_10574_b200.storage import CSF3
+
+        B = self.cfg["B"]
+        f = int(B.pos1[slices])
+        z = int(B.pos2[f])
+        sub = CSF3((slices, B.dims[1], B.dims[2]), B.pos1[: slices + 1], B.idx1[:f],
+                   B.pos2[: f + 1], B.idx2[:z], B.vals[:z])
+        return sub
+
+    def ref_run(self, sub, nthreads):
+        import oracle
+
+        if self.dense:
+            oracle.ref_mttkrp_dense(sub, self.cfg["C"].vals, self.cfg["D"].vals, nthreads)
+            nbytes = _csf_bytes(sub) + 8 * (self.cfg["C"].vals.size + self.cfg["D"].vals.size) + \
+                8 * sub.dims[0] * self.R
+            return nbytes, 2 * self.R * (sub.nnz + sub.nfibers)
+        out = oracle.ref_mttkrp_sparse(sub, self.cfg["C"], self.cfg["D"], nthreads)
+        nbytes = _csf_bytes(sub) + _csr_bytes(self.cfg["C"]) + _csr_bytes(self.cfg["D"]) + \
+            8 * (out["nrows"] + 1) + 16 * int(out["pos"][-1])
+        return nbytes, 0
+
+    def total_rows(self):
+        return self.cfg["B"].dims[0]
+
+
+WORKLOADS = {1: SpgemmWork, 2: SpaddWork, 3: SpgemmWork, 4: MttkrpWork, 5: MttkrpWork}
 
 
 # ---------------------------------------------------------------------------

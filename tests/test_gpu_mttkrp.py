@@ -1,0 +1,120 @@
+"""GPU parity: CSF MTTKRP (dense and sparse result) vs the CPU oracle.
+
+Values within |x - x_ref| <= 1e-12 * max(|x_ref|, s_ref), s_ref the sum of
+|terms| (reordering 6k-term sums breaks a per-entry 1e-12
+relative bound, the scaled bound holds); sparse-result structure bit-exact
+(presence-checked w0)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1802_10574_b200 import CSF3, CSR, Dense, StamError
+from paper_1802_10574_b200 import generators as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _dense_ok(A, ref, tol=1e-12):
+    got = A.numpy() if isinstance(A, Dense) else np.asarray(A)
+    err = np.abs(got - ref["vals"])
+    bound = tol * np.maximum(np.abs(ref["vals"]), ref["abs"])
+    assert np.all(err <= bound), f"{int(np.sum(err > bound))} entries out of tolerance"
+
+
+def _d(x):
+    return x.to("cuda")
+
+
+@pytest.mark.parametrize("scale", [0.005, 0.05])
+def test_mttkrp_dense_config4_scaled(ctx, scale):
+    cfg = G.make_config(4, scale=scale)
+    A = ctx.mttkrp(_d(cfg["B"]), _d(cfg["C"]), _d(cfg["D"]))
+    _dense_ok(A, oracle.mttkrp_dense(cfg["B"], cfg["C"].vals, cfg["D"].vals, 8))
+
+
+@pytest.mark.slow
+def test_mttkrp_dense_config4_full(ctx):
+    cfg = G.make_config(4)
+    A = ctx.mttkrp(_d(cfg["B"]), _d(cfg["C"]), _d(cfg["D"]))
+    _dense_ok(A, oracle.mttkrp_dense(cfg["B"], cfg["C"].vals, cfg["D"].vals,
+                                     oracle.threads_default()))
+
+
+@pytest.mark.parametrize("R", [1, 7, 32, 33, 64, 100])
+def test_mttkrp_dense_ranks(ctx, R):
+    sizes = G.slice_sizes_ranksize(300, 20000, 1.5, 5)
+    B = G.csf3((300, 200, 400), sizes, 6)
+    C = G.dense(200, R, 7)
+    D = G.dense(400, R, 8)
+    A = ctx.mttkrp(_d(B), _d(C), _d(D))
+    _dense_ok(A, oracle.mttkrp_dense(B, C.vals, D.vals))
+
+
+def test_mttkrp_dense_empty_slices_and_long_fibers(ctx):
+    # one slice with very long fibers (crosses many chunks), empty slices
+    sizes = np.zeros(50, dtype=np.int64)
+    sizes[[3, 10, 11, 40]] = [200_000, 5, 1, 3000]
+    B = G.csf3((50, 20, 100_000), sizes, 9)
+    C, D = G.dense(20, 32, 10), G.dense(100_000, 32, 11)
+    A = ctx.mttkrp(_d(B), _d(C), _d(D))
+    ref = oracle.mttkrp_dense(B, C.vals, D.vals)
+    _dense_ok(A, ref)
+    assert np.all(ref["vals"][[0, 1, 2, 49]] == 0)
+
+
+def test_mttkrp_dense_matches_dense_einsum(ctx):
+    rng = np.random.default_rng(1)
+    t = rng.random((6, 5, 7)) * (rng.random((6, 5, 7)) < 0.3)
+    C, D = rng.random((5, 4)), rng.random((7, 4))
+    A = ctx.mttkrp(_d(CSF3.from_dense(t)), _d(Dense(C)), _d(Dense(D)), result="host")
+    np.testing.assert_allclose(A.numpy(), np.einsum("ijk,jr,kr->ir", t, C, D), rtol=1e-12,
+                               atol=1e-14)
+
+
+def test_mttkrp_dense_deterministic(ctx):
+    cfg = G.make_config(4, scale=0.02)
+    args = (_d(cfg["B"]), _d(cfg["C"]), _d(cfg["D"]))
+    a1 = ctx.mttkrp(*args).numpy()
+    a2 = ctx.mttkrp(*args).numpy()
+    assert np.array_equal(a1.view(np.int64), a2.view(np.int64))
+
+
+@pytest.mark.parametrize("scale", [0.0005, 0.005])
+def test_mttkrp_sparse_config5_scaled(ctx, scale):
+    cfg = G.make_config(5, scale=scale)
+    A = ctx.mttkrp(_d(cfg["B"]), _d(cfg["C"]), _d(cfg["D"]))
+    oracle.compare_csr(A, oracle.mttkrp_sparse(cfg["B"], cfg["C"], cfg["D"], 8))
+
+
+def test_mttkrp_sparse_multi_nonzero_fibers(ctx):
+    # dense-ish slices: fibers with many k, factors with many columns per row
+    sizes = np.full(40, 600, dtype=np.int64)
+    B = G.csf3((40, 30, 50), sizes, 12)
+    C = G.csr_fixed(30, 96, 40, 13)
+    D = G.csr_fixed(50, 96, 25, 14)
+    A = ctx.mttkrp(_d(B), _d(C), _d(D))
+    oracle.compare_csr(A, oracle.mttkrp_sparse(B, C, D))
+
+
+def test_mttkrp_sparse_matches_dense_where_present(ctx):
+    rng = np.random.default_rng(2)
+    t = rng.random((5, 6, 7)) * (rng.random((5, 6, 7)) < 0.4)
+    c = rng.random((6, 9)) * (rng.random((6, 9)) < 0.5)
+    d = rng.random((7, 9)) * (rng.random((7, 9)) < 0.5)
+    A = ctx.mttkrp(_d(CSF3.from_dense(t)), _d(CSR.from_dense(c)), _d(CSR.from_dense(d)),
+                   result="host")
+    np.testing.assert_allclose(A.to_dense(), np.einsum("ijk,jr,kr->ir", t, c, d), rtol=1e-12,
+                               atol=1e-14)
+
+
+def test_mttkrp_mixed_factors_rejected(ctx):
+    cfg = G.make_config(4, scale=0.005)
+    with pytest.raises(StamError):
+        ctx.mttkrp(_d(cfg["B"]), _d(cfg["C"]), CSR.from_dense(np.eye(3)))
+
+
+def test_mttkrp_dimension_mismatch(ctx):
+    cfg = G.make_config(4, scale=0.005)
+    with pytest.raises(StamError) as e:
+        ctx.mttkrp(_d(cfg["B"]), _d(cfg["D"]), _d(cfg["C"]))
+    assert e.value.code == "DimensionMismatch"
