@@ -51,7 +51,10 @@ struct DenseParams {
   double* A;        // I x R (zeroed)
   int64_t chunk_nnz;
   int64_t nchunks;
-  double* part;       // [ncb][nchunks][2][32] partials (head, tail)
+  int64_t* chunk_fa;    // [nchunks+1] first fiber starting in chunk c
+  int64_t* chunk_s;     // [nchunks+1] slice of chunk_fa[c] (I when none)
+  unsigned long long* counter;  // dynamic chunk claims
+  double* part;         // [ncb][nchunks][2][32] partials (head, tail)
   int64_t* part_slice;  // [nchunks][2]: head slice (-1 none, -2 empty chunk), tail slice
 };
 
@@ -79,33 +82,170 @@ __device__ __forceinline__ int64_t slice_of(const int64_t* pos1, int64_t I, int6
   return lo;
 }
 
-// Column-block pass of 32 columns starting at cb.  kVec: lanes hold double2
-// (half-warp per nonzero, two nonzeros per step) when R is even and the rows
-// are 16-byte aligned; otherwise a full warp per nonzero, one double per lane.
-template <bool kVec>
-struct Lanes {
-  static constexpr int kPerStep = kVec ? 2 : 1;
+// Chunk c owns the fibers whose first nonzero lies in [c*S, (c+1)*S).
+__global__ void mttkrp_dense_bounds_kernel(const DenseParams P) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > P.nchunks) return;
+  const int64_t fa = c == P.nchunks ? P.nfibers : lower_bound_g(P.pos2, P.nfibers, c * P.chunk_nnz);
+  P.chunk_fa[c] = fa;
+  P.chunk_s[c] = fa < P.nfibers ? slice_of(P.pos1, P.I, fa) : P.I;
+}
+
+// Per-chunk slice bookkeeping shared by both dense kernels: slices that start
+// and end inside the chunk are stored directly; the chunk's first slice, if it
+// began earlier, leaves a head partial; its last slice, if it continues,
+// leaves a tail partial (or the head partial when it is also the first).
+struct SliceTracker {
+  int64_t s, s_end;
+  bool open;        // current slice began before this chunk
+  bool wrote_head;
 };
 
-template <bool kVec>
-__global__ void __launch_bounds__(256) mttkrp_dense_kernel(const DenseParams P) {
+// R == 32 with 16-byte aligned rows: two half-warps take alternate nonzeros
+// of a fiber and read D rows as double2 (a row = 16 lanes x 16 B); up to 8
+// independent row loads in flight per lane; the next fiber's first (k, b)
+// batch and its C row are issued before the current fiber is reduced.
+__global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParams P) {
   const int lane = (int)lane_id();
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int half = lane >> 4;
+  const int col = 2 * (lane & 15);
+  while (true) {
+    int64_t c = 0;
+    if (lane == 0) c = (int64_t)atomicAdd(P.counter, 1ull);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= P.nchunks) break;
+    const int64_t fa = P.chunk_fa[c], fb = P.chunk_fa[c + 1];
+    double* part = P.part + (c * 2) * 32;
+    if (fa >= fb) {
+      if (lane == 0) {
+        P.part_slice[2 * c] = -2;
+        P.part_slice[2 * c + 1] = -1;
+      }
+      continue;
+    }
+    SliceTracker st;
+    st.s = P.chunk_s[c];
+    st.s_end = P.pos1[st.s + 1];
+    st.open = P.pos1[st.s] < fa;
+    st.wrote_head = false;
+    double acc0 = 0.0, acc1 = 0.0;
+    auto flush = [&](bool ends_here) {
+      const bool started_here = !st.open;
+      if (started_here && ends_here) {
+        if (half == 0)
+          reinterpret_cast<double2*>(P.A + st.s * 32 + col)[0] = make_double2(acc0, acc1);
+      } else {
+        const int slot = started_here ? 1 : 0;
+        if (half == 0) reinterpret_cast<double2*>(part + slot * 32 + col)[0] = make_double2(acc0, acc1);
+        if (lane == 0) P.part_slice[2 * c + slot] = st.s;
+        if (slot == 0) st.wrote_head = true;
+      }
+      acc0 = 0.0;
+      acc1 = 0.0;
+    };
+    for (int64_t fg = fa; fg < fb; fg += 32) {
+      const int nf = (int)min((int64_t)32, fb - fg);
+      int64_t mj = 0, mz = 0, mz1 = 0;
+      if (lane < nf) {
+        mj = P.idx1[fg + lane];
+        mz = P.pos2[fg + lane];
+        mz1 = P.pos2[fg + lane + 1];
+      }
+      // first batch of fiber 0 of the group
+      int64_t z0 = __shfl_sync(kFull, mz, 0);
+      int64_t z1 = __shfl_sync(kFull, mz1, 0);
+      int kz = 0;
+      double bz = 0.0;
+      if (lane < z1 - z0) {
+        kz = (int)P.idx2[z0 + lane];
+        bz = P.vals[z0 + lane];
+      }
+      int64_t jn = __shfl_sync(kFull, mj, 0);
+      double2 cj = __ldg(reinterpret_cast<const double2*>(P.C + jn * 32 + col));
+      for (int t = 0; t < nf; t++) {
+        const int64_t f = fg + t;
+        while (f >= st.s_end) {
+          st.s++;
+          st.s_end = P.pos1[st.s + 1];
+          st.open = false;
+        }
+        const int64_t cz0 = z0, cz1 = z1;
+        int ckz = kz;
+        double cbz = bz;
+        const double2 ccj = cj;
+        // prefetch the next fiber's first batch and C row
+        if (t + 1 < nf) {
+          z0 = __shfl_sync(kFull, mz, t + 1);
+          z1 = __shfl_sync(kFull, mz1, t + 1);
+          kz = 0;
+          bz = 0.0;
+          if (lane < z1 - z0) {
+            kz = (int)P.idx2[z0 + lane];
+            bz = P.vals[z0 + lane];
+          }
+          jn = __shfl_sync(kFull, mj, t + 1);
+          cj = __ldg(reinterpret_cast<const double2*>(P.C + jn * 32 + col));
+        }
+        double w0 = 0.0, w1 = 0.0;
+        for (int64_t zb = cz0; zb < cz1; zb += 32) {
+          const int n = (int)min((int64_t)32, cz1 - zb);
+          if (zb != cz0) {
+            ckz = 0;
+            cbz = 0.0;
+            if (lane < n) {
+              ckz = (int)P.idx2[zb + lane];
+              cbz = P.vals[zb + lane];
+            }
+          }
+          for (int t0 = 0; t0 < n; t0 += 16) {
+            double2 d[8];
+            double b[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+              const int src = t0 + 2 * u + half;
+              const int k = __shfl_sync(kFull, ckz, src & 31);
+              const double bv = __shfl_sync(kFull, cbz, src & 31);
+              const bool ok = src < n;
+              b[u] = ok ? bv : 0.0;
+              d[u] = ok ? __ldg(reinterpret_cast<const double2*>(P.D + (int64_t)k * 32 + col))
+                        : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+              w0 = fma(b[u], d[u].x, w0);
+              w1 = fma(b[u], d[u].y, w1);
+            }
+          }
+        }
+        w0 += __shfl_xor_sync(kFull, w0, 16);
+        w1 += __shfl_xor_sync(kFull, w1, 16);
+        acc0 = fma(w0, ccj.x, acc0);
+        acc1 = fma(w1, ccj.y, acc1);
+        if (f + 1 == st.s_end) flush(true);
+      }
+    }
+    if (fb < st.s_end) flush(false);
+    if (lane == 0) {
+      if (!st.wrote_head) P.part_slice[2 * c] = -1;
+      if (!(fb < st.s_end && !st.open)) P.part_slice[2 * c + 1] = -1;
+    }
+  }
+}
+
+// Any R: column blocks of 32, a full warp per nonzero, one double per lane.
+__global__ void __launch_bounds__(256) mttkrp_dense_generic_kernel(const DenseParams P) {
+  const int lane = (int)lane_id();
   const int64_t ncb = (P.R + 31) / 32;
-  // lane geometry
-  const int half = kVec ? (lane >> 4) : 0;
-  const int hl = kVec ? (lane & 15) : lane;
-  for (int64_t task = gwarp; task < P.nchunks * ncb; task += nwarps) {
+  while (true) {
+    int64_t task = 0;
+    if (lane == 0) task = (int64_t)atomicAdd(P.counter, 1ull);
+    task = __shfl_sync(kFull, task, 0);
+    if (task >= P.nchunks * ncb) break;
     const int64_t c = task % P.nchunks;
     const int64_t cbi = task / P.nchunks;
-    const int64_t cb = cbi * 32;
-    // columns held by this lane: kVec -> cb + 2*hl, +1 ; else cb + hl
-    const int64_t col = kVec ? cb + 2 * hl : cb + hl;
+    const int64_t col = cbi * 32 + lane;
     const bool col_ok = col < P.R;
-    // fiber range of the chunk: fibers whose first nonzero lies in it
-    const int64_t fa = lower_bound_g(P.pos2, P.nfibers, c * P.chunk_nnz);
-    const int64_t fb = lower_bound_g(P.pos2, P.nfibers, (c + 1) * P.chunk_nnz);
+    const int64_t fa = P.chunk_fa[c], fb = P.chunk_fa[c + 1];
     double* part = P.part + ((cbi * P.nchunks + c) * 2) * 32;
     if (fa >= fb) {
       if (lane == 0 && cbi == 0) {
@@ -114,48 +254,33 @@ __global__ void __launch_bounds__(256) mttkrp_dense_kernel(const DenseParams P) 
       }
       continue;
     }
-    int64_t s = slice_of(P.pos1, P.I, fa);
-    int64_t s_end = P.pos1[s + 1];
-    const int64_t head_slice = s;
-    bool head_open = P.pos1[s] < fa;  // first slice began in an earlier chunk
-    bool wrote_head = false;
-    double acc0 = 0.0, acc1 = 0.0;
-    auto flush = [&](int64_t sl, bool started_here, bool ends_here) {
-      // combine halves: both halves accumulated the same w0*C, only half 0 writes
+    SliceTracker st;
+    st.s = P.chunk_s[c];
+    st.s_end = P.pos1[st.s + 1];
+    st.open = P.pos1[st.s] < fa;
+    st.wrote_head = false;
+    double acc = 0.0;
+    auto flush = [&](bool ends_here) {
+      const bool started_here = !st.open;
       if (started_here && ends_here) {
-        if (col_ok && half == 0) {
-          if (kVec) {
-            reinterpret_cast<double2*>(P.A + sl * P.R + col)[0] = make_double2(acc0, acc1);
-          } else {
-            P.A[sl * P.R + col] = acc0;
-          }
-        }
+        if (col_ok) P.A[st.s * P.R + col] = acc;
       } else {
-        // partial: head (slot 0) if it began before this chunk, else tail (slot 1)
         const int slot = started_here ? 1 : 0;
-        if (half == 0) {
-          if (kVec) {
-            part[slot * 32 + 2 * hl] = acc0;
-            part[slot * 32 + 2 * hl + 1] = acc1;
-          } else {
-            part[slot * 32 + hl] = acc0;
-          }
-        }
-        if (lane == 0 && cbi == 0) P.part_slice[2 * c + slot] = sl;
-        if (slot == 0) wrote_head = true;
+        part[slot * 32 + lane] = acc;
+        if (lane == 0 && cbi == 0) P.part_slice[2 * c + slot] = st.s;
+        if (slot == 0) st.wrote_head = true;
       }
-      acc0 = 0.0;
-      acc1 = 0.0;
+      acc = 0.0;
     };
     for (int64_t f = fa; f < fb; f++) {
-      while (f >= s_end) {  // next non-empty slice
-        s++;
-        s_end = P.pos1[s + 1];
-        head_open = false;
+      while (f >= st.s_end) {
+        st.s++;
+        st.s_end = P.pos1[st.s + 1];
+        st.open = false;
       }
       const int64_t j = P.idx1[f];
       const int64_t z0 = P.pos2[f], z1 = P.pos2[f + 1];
-      double w0 = 0.0, w1 = 0.0;
+      double w = 0.0;
       for (int64_t zb = z0; zb < z1; zb += 32) {
         const int n = (int)min((int64_t)32, z1 - zb);
         int kz = 0;
@@ -164,72 +289,74 @@ __global__ void __launch_bounds__(256) mttkrp_dense_kernel(const DenseParams P) 
           kz = (int)P.idx2[zb + lane];
           bz = P.vals[zb + lane];
         }
-        const int steps = (n + Lanes<kVec>::kPerStep - 1) / Lanes<kVec>::kPerStep;
-#pragma unroll 4
-        for (int t = 0; t < steps; t++) {
-          const int src = t * Lanes<kVec>::kPerStep + half;
-          const int k = __shfl_sync(kFull, kz, src & 31);
-          double b = __shfl_sync(kFull, bz, src & 31);
-          if (src >= n) b = 0.0;
-          if (col_ok) {
-            if (kVec) {
-              const double2 d = __ldg(reinterpret_cast<const double2*>(P.D + (int64_t)k * P.R + col));
-              w0 = fma(b, d.x, w0);
-              w1 = fma(b, d.y, w1);
-            } else {
-              w0 = fma(b, __ldg(P.D + (int64_t)k * P.R + col), w0);
-            }
+        for (int t0 = 0; t0 < n; t0 += 8) {
+          double d[8], b[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int src = t0 + u;
+            const int k = __shfl_sync(kFull, kz, src & 31);
+            const double bv = __shfl_sync(kFull, bz, src & 31);
+            const bool ok = src < n && col_ok;
+            b[u] = ok ? bv : 0.0;
+            d[u] = ok ? __ldg(P.D + (int64_t)k * P.R + col) : 0.0;
           }
+#pragma unroll
+          for (int u = 0; u < 8; u++) w = fma(b[u], d[u], w);
         }
       }
-      if (kVec) {
-        w0 += __shfl_xor_sync(kFull, w0, 16);
-        w1 += __shfl_xor_sync(kFull, w1, 16);
-      }
-      if (col_ok) {
-        if (kVec) {
-          const double2 cj = __ldg(reinterpret_cast<const double2*>(P.C + j * P.R + col));
-          acc0 = fma(w0, cj.x, acc0);
-          acc1 = fma(w1, cj.y, acc1);
-        } else {
-          acc0 = fma(w0, __ldg(P.C + j * P.R + col), acc0);
-        }
-      }
-      // slice ends inside this chunk?
-      if (f + 1 == s_end) flush(s, !head_open, true);
+      if (col_ok) acc = fma(w, __ldg(P.C + j * P.R + col), acc);
+      if (f + 1 == st.s_end) flush(true);
     }
-    // the last slice continues past the chunk
-    if (fb < s_end) flush(s, !head_open, false);
+    if (fb < st.s_end) flush(false);
     if (lane == 0 && cbi == 0) {
-      if (!wrote_head) P.part_slice[2 * c] = -1;
-      // tail slot written only when the last slice started here and continues
-      if (!(fb < s_end && !head_open)) P.part_slice[2 * c + 1] = -1;
+      if (!st.wrote_head) P.part_slice[2 * c] = -1;
+      if (!(fb < st.s_end && !st.open)) P.part_slice[2 * c + 1] = -1;
     }
-    (void)head_slice;
   }
 }
 
-// Sums the partials of every slice cut by chunk boundaries, in chunk order.
-__global__ void mttkrp_dense_fixup_kernel(const DenseParams P) {
+// Sums the partials of every slice cut by chunk boundaries, in a fixed order:
+// one CTA per chain (the chunk holding the slice's tail partial plus the
+// following chunks holding its head partials); 8 warps take strided chunks,
+// then the 8 warp sums are added in warp order (deterministic).
+constexpr int kFixThreads = 256;
+__global__ void __launch_bounds__(kFixThreads) mttkrp_dense_fixup_kernel(const DenseParams P) {
+  __shared__ int64_t end_sh;
+  __shared__ double red[kFixThreads / 32][32];
   const int lane = (int)lane_id();
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int warp = threadIdx.x >> 5;
   const int64_t ncb = (P.R + 31) / 32;
-  for (int64_t task = gwarp; task < P.nchunks * ncb; task += nwarps) {
-    const int64_t c = task % P.nchunks;
-    const int64_t cbi = task / P.nchunks;
+  for (int64_t c = blockIdx.x; c < P.nchunks; c += gridDim.x) {
     const int64_t s = P.part_slice[2 * c + 1];
-    if (s < 0) continue;  // this chunk does not start a cut slice
-    const int64_t col = cbi * 32 + lane;
-    const double* base = P.part + cbi * P.nchunks * 64;
-    double sum = base[(c * 2 + 1) * 32 + lane];
-    for (int64_t c2 = c + 1; c2 < P.nchunks; c2++) {
-      const int64_t h = P.part_slice[2 * c2];
-      if (h == -2) continue;  // empty chunk (inside a long fiber)
-      if (h != s) break;
-      sum += base[(c2 * 2) * 32 + lane];
+    if (s < 0) continue;  // uniform across the CTA
+    // chain end: first chunk after c whose head is neither s nor an empty chunk
+    if (threadIdx.x == 0) end_sh = P.nchunks;
+    __syncthreads();
+    for (int64_t base = c + 1; base < P.nchunks; base += kFixThreads) {
+      const int64_t t = base + threadIdx.x;
+      if (t < P.nchunks) {
+        const int64_t h = P.part_slice[2 * t];
+        if (h != s && h != -2) atomicMin((long long*)&end_sh, (long long)t);
+      }
+      __syncthreads();
+      if (end_sh < P.nchunks) break;
     }
-    if (col < P.R) P.A[s * P.R + col] = sum;
+    const int64_t e = end_sh;
+    for (int64_t cbi = 0; cbi < ncb; cbi++) {
+      const double* base = P.part + cbi * P.nchunks * 64;
+      double sum = 0.0;
+      for (int64_t c2 = c + 1 + warp; c2 < e; c2 += kFixThreads / 32)
+        if (P.part_slice[2 * c2] == s) sum += base[(c2 * 2) * 32 + lane];
+      red[warp][lane] = sum;
+      __syncthreads();
+      if (warp == 0) {
+        double total = base[(c * 2 + 1) * 32 + lane];
+        for (int w = 0; w < kFixThreads / 32; w++) total += red[w][lane];
+        const int64_t col = cbi * 32 + lane;
+        if (col < P.R) P.A[s * P.R + col] = total;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -237,8 +364,8 @@ __global__ void mttkrp_dense_fixup_kernel(const DenseParams P) {
 // sparse
 // ===========================================================================
 constexpr int kSpWarps = 8;
-constexpr int kSpSlicesPerWarp = 2;
-constexpr int kSpTile = kSpWarps * kSpSlicesPerWarp;
+constexpr int kSpSlicesPerWarp = 2;  // slices per warp-level tile
+constexpr int kRowChunk = 8;         // factor-row entries held in registers at once
 
 struct SparseParams {
   int64_t I, R;
@@ -277,6 +404,11 @@ __device__ __forceinline__ int64_t locate(const int64_t* a, int64_t n, int64_t x
   return (lo < n && a[lo] == x) ? lo : -1;
 }
 
+__device__ __forceinline__ void ws_add(double* wv, uint32_t* wb, int64_t r, double v) {
+  atomicAdd(&wv[r], v);
+  atomicOr(&wb[r >> 5], 1u << (r & 31));
+}
+
 // Evaluates slice i into the warp's workspace (vals[R], bits[R/32]).
 __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint32_t* wb) {
   const int lane = (int)lane_id();
@@ -286,25 +418,31 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
     const int64_t z0 = P.pos2[f], z1 = P.pos2[f + 1];
     const int64_t c0 = P.cpos[j], c1 = P.cpos[j + 1];
     if (z1 - z0 == 1) {
-      // single nonzero: intersect C_j with D_k by merging the sorted rows
+      // single nonzero: C_j ∩ D_k.  Column ids of both rows are loaded into
+      // registers kRowChunk at a time (independent loads) and intersected
+      // all-pairs; values are fetched only for matches.
       const int64_t k = P.idx2[z0];
       const double b = P.vals[z0];
-      int64_t d = P.dpos[k];
-      const int64_t d1 = P.dpos[k + 1];
-      int64_t q = c0;
-      while (q < c1 && d < d1) {
-        const int64_t rc = P.cidx[q], rd = P.didx[d];
-        if (rc < rd) {
-          q++;
-        } else if (rd < rc) {
-          d++;
-        } else {
-          // w0(r) = 0 + b*D(k,r);  w1(r) += w0(r)*C(j,r)
-          const double w0 = add_rn(0.0, mul_rn(b, P.dvals[d]));
-          atomicAdd(&wv[rc], mul_rn(w0, P.cvals[q]));
-          atomicOr(&wb[rc >> 5], 1u << (rc & 31));
-          q++;
-          d++;
+      const int64_t d0 = P.dpos[k], d1 = P.dpos[k + 1];
+      for (int64_t cq = c0; cq < c1; cq += kRowChunk) {
+        int cc[kRowChunk];
+#pragma unroll
+        for (int a = 0; a < kRowChunk; a++) cc[a] = cq + a < c1 ? (int)P.cidx[cq + a] : -1;
+        for (int64_t dq = d0; dq < d1; dq += kRowChunk) {
+          int dd[kRowChunk];
+#pragma unroll
+          for (int e = 0; e < kRowChunk; e++) dd[e] = dq + e < d1 ? (int)P.didx[dq + e] : -2;
+#pragma unroll
+          for (int a = 0; a < kRowChunk; a++) {
+            int hit = -1;
+#pragma unroll
+            for (int e = 0; e < kRowChunk; e++) hit = (dd[e] == cc[a]) ? e : hit;
+            if (hit >= 0) {
+              // w0(r) = 0 + b*D(k,r);  w1(r) += w0(r)*C(j,r)
+              const double w0 = add_rn(0.0, mul_rn(b, P.dvals[dq + hit]));
+              ws_add(wv, wb, cc[a], mul_rn(w0, P.cvals[cq + a]));
+            }
+          }
         }
       }
     } else {
@@ -322,83 +460,75 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
             present = true;
           }
         }
-        if (present) {
-          atomicAdd(&wv[r], mul_rn(w0, P.cvals[q]));
-          atomicOr(&wb[r >> 5], 1u << (r & 31));
-        }
+        if (present) ws_add(wv, wb, r, mul_rn(w0, P.cvals[q]));
       }
     }
   }
 }
 
+// Warp-level ordered tiles: each warp claims a tile of kSpSlicesPerWarp
+// slices, evaluates them, looks back for its output offset and drains.
 __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const SparseParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int64_t tile_sh;
-  __shared__ int64_t cnt_sh[kSpTile];
-  __shared__ int64_t dst_sh[kSpTile];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
   const int64_t R = P.R;
   const int nwords = (int)((R + 31) / 32);
-  // per warp: kSpSlicesPerWarp workspaces of R doubles + nwords bitmap words
-  const size_t ws_bytes = (size_t)R * 8 + (size_t)nwords * 4;
-  unsigned char* wbase = smem_raw + (size_t)warp * kSpSlicesPerWarp * ((ws_bytes + 15) & ~(size_t)15);
-  if (threadIdx.x == 0) tile_sh = (int64_t)atomicAdd(P.tile_counter, 1ull);
-  __syncthreads();
-  const int64_t tile = tile_sh;
-  const int64_t i0 = tile * kSpTile;
-  for (int k = 0; k < kSpSlicesPerWarp; k++) {
-    const int t = warp * kSpSlicesPerWarp + k;
-    const int64_t i = i0 + t;
-    double* wv = reinterpret_cast<double*>(wbase + k * ((ws_bytes + 15) & ~(size_t)15));
-    uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
-    for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
-    for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
-    __syncwarp();
-    int64_t cnt = 0;
-    if (i < P.I) {
-      sparse_slice(P, i, wv, wb);
+  const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
+  unsigned char* wbase = smem_raw + (size_t)warp * kSpSlicesPerWarp * ws_bytes;
+  while (true) {
+    int64_t tile = 0;
+    if (lane == 0) tile = (int64_t)atomicAdd(P.tile_counter, 1ull);
+    tile = __shfl_sync(kFull, tile, 0);
+    if (tile >= P.ntiles) break;
+    const int64_t i0 = tile * kSpSlicesPerWarp;
+    int64_t cnt[kSpSlicesPerWarp];
+#pragma unroll
+    for (int k = 0; k < kSpSlicesPerWarp; k++) {
+      double* wv = reinterpret_cast<double*>(wbase + k * ws_bytes);
+      uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
+      for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
+      for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
       __syncwarp();
-      for (int w = lane; w < nwords; w += 32) cnt += __popc(wb[w]);
-      cnt = warp_sum(cnt);
-    }
-    if (lane == 0) cnt_sh[t] = cnt;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int64_t c = lane < kSpTile ? cnt_sh[lane] : 0;
-    const int64_t inc = warp_inclusive_scan(c);
-    const int64_t agg = __shfl_sync(kFull, inc, 31);
-    const int64_t base = lookback_exclusive(P.tile_status, tile, agg);
-    if (lane < kSpTile) {
-      dst_sh[lane] = base + inc - c;
-      if (i0 + lane < P.I) P.out_pos[i0 + lane + 1] = base + inc;
-    }
-    if (lane == 0) {
-      if (tile == 0) P.out_pos[0] = 0;
-      if (tile == P.ntiles - 1) *P.total_nnz = base + agg;
-    }
-  }
-  __syncthreads();
-  // drain: sorted by ballot/popcount over the presence bitmap
-  for (int k = 0; k < kSpSlicesPerWarp; k++) {
-    const int t = warp * kSpSlicesPerWarp + k;
-    if (i0 + t >= P.I) continue;
-    const double* wv = reinterpret_cast<double*>(wbase + k * ((ws_bytes + 15) & ~(size_t)15));
-    const uint32_t* wb = reinterpret_cast<const uint32_t*>(wv + R);
-    int64_t out = dst_sh[t];
-    for (int w = 0; w < nwords; w++) {
-      const uint32_t bits = wb[w];
-      if (bits == 0) continue;
-      const bool mine = (bits >> lane) & 1u;
-      if (mine) {
-        const int rank = __popc(bits & ((1u << lane) - 1u));
-        const int64_t r = (int64_t)w * 32 + lane;
-        P.out_idx[out + rank] = r;
-        P.out_vals[out + rank] = wv[r];
+      cnt[k] = 0;
+      if (i0 + k < P.I) {
+        sparse_slice(P, i0 + k, wv, wb);
+        __syncwarp();
+        int64_t c = 0;
+        for (int w = lane; w < nwords; w += 32) c += __popc(wb[w]);
+        cnt[k] = warp_sum(c);
       }
-      out += __popc(bits);
     }
+    int64_t agg = 0;
+#pragma unroll
+    for (int k = 0; k < kSpSlicesPerWarp; k++) agg += cnt[k];
+    const int64_t base = lookback_exclusive(P.tile_status, tile, agg);
+    int64_t out = base;
+#pragma unroll
+    for (int k = 0; k < kSpSlicesPerWarp; k++) {
+      const int64_t i = i0 + k;
+      if (i >= P.I) break;
+      if (lane == 0) {
+        if (i == 0) P.out_pos[0] = 0;
+        P.out_pos[i + 1] = out + cnt[k];
+      }
+      const double* wv = reinterpret_cast<double*>(wbase + k * ws_bytes);
+      const uint32_t* wb = reinterpret_cast<const uint32_t*>(wv + R);
+      // sorted drain by ballot/popcount over the presence bitmap
+      for (int w = 0; w < nwords; w++) {
+        const uint32_t bits = wb[w];
+        if (bits == 0) continue;
+        if ((bits >> lane) & 1u) {
+          const int rank = __popc(bits & ((1u << lane) - 1u));
+          const int64_t r = (int64_t)w * 32 + lane;
+          P.out_idx[out + rank] = r;
+          P.out_vals[out + rank] = wv[r];
+        }
+        out += __popc(bits);
+      }
+    }
+    if (lane == 0 && tile == P.ntiles - 1) *P.total_nnz = base + agg;
+    __syncwarp();
   }
 }
 
@@ -441,24 +571,31 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
     P.A = A->vals;
     STAM_CUDA_CHECK(cudaMemsetAsync(P.A, 0, sizeof(double) * (size_t)(I * R), call.stream()));
     const int sms = call.ctx()->num_sms;
-    const int64_t warps = (int64_t)sms * 64;
     const int64_t ncb = (R + 31) / 32;
-    P.chunk_nnz = std::max<int64_t>(256, ceil_div(std::max<int64_t>(B->nnz, 1), warps * 2));
+    const bool fast = R == 32 && ((uintptr_t)P.C % 16 == 0) && ((uintptr_t)P.D % 16 == 0);
+    // ~16 chunks per resident warp: small enough to balance the skewed
+    // slices, large enough to amortize a chunk's bookkeeping
+    const int64_t warps = (int64_t)sms * 32;
+    P.chunk_nnz = std::max<int64_t>(512, ceil_div(std::max<int64_t>(B->nnz, 1), warps * 16));
     P.nchunks = std::max<int64_t>(1, ceil_div(B->nnz, P.chunk_nnz));
     P.part = call.scratch_n<double>((size_t)(ncb * P.nchunks * 64));
     P.part_slice = call.scratch_n<int64_t>((size_t)(2 * P.nchunks));
-    const bool vec = (R % 2 == 0) && ((uintptr_t)P.C % 16 == 0) && ((uintptr_t)P.D % 16 == 0);
-    const int64_t tasks = P.nchunks * ncb;
-    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(tasks, 8), (int64_t)sms * 8);
+    P.chunk_fa = call.scratch_n<int64_t>((size_t)P.nchunks + 1);
+    P.chunk_s = call.scratch_n<int64_t>((size_t)P.nchunks + 1);
+    P.counter = static_cast<unsigned long long*>(call.scratch_zero(16));
     if (B->nfibers > 0) {
-      call.before_launch("mttkrp_dense");
-      if (vec)
-        mttkrp_dense_kernel<true><<<grid, 256, 0, call.stream()>>>(P);
+      call.before_launch("mttkrp_dense_bounds");
+      mttkrp_dense_bounds_kernel<<<(unsigned)ceil_div(P.nchunks + 1, 256), 256, 0, call.stream()>>>(P);
+      call.after_launch();
+      call.before_launch(fast ? "mttkrp_dense32" : "mttkrp_dense_generic");
+      if (fast)
+        mttkrp_dense32_kernel<<<(unsigned)(sms * 3), 256, 0, call.stream()>>>(P);
       else
-        mttkrp_dense_kernel<false><<<grid, 256, 0, call.stream()>>>(P);
+        mttkrp_dense_generic_kernel<<<(unsigned)(sms * 4), 256, 0, call.stream()>>>(P);
       call.after_launch();
       call.before_launch("mttkrp_dense_fixup");
-      mttkrp_dense_fixup_kernel<<<grid, 256, 0, call.stream()>>>(P);
+      mttkrp_dense_fixup_kernel<<<(unsigned)std::min<int64_t>(P.nchunks, (int64_t)sms * 8),
+                                  kFixThreads, 0, call.stream()>>>(P);
       call.after_launch();
     }
     call.finish_dense_result(A);
@@ -505,7 +642,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.dpos = call.device_input(Dv->pos, (size_t)Dv->nrows + 1, Dv->mem);
     P.didx = call.device_input(Dv->idx, (size_t)Dv->nnz, Dv->mem);
     P.dvals = call.device_input(Dv->vals, (size_t)Dv->nnz, Dv->mem);
-    P.ntiles = ceil_div(I, kSpTile);
+    P.ntiles = ceil_div(I, kSpSlicesPerWarp);
     // a row of A has at most R entries: I*R bounds the output (no counting pass)
     const int64_t bound = I * R;
     call.alloc_csr_result(A, I, R, std::min<int64_t>(bound, (int64_t)1 << 40));
@@ -518,8 +655,13 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.tile_status = ctl + 4;
     STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mttkrp_sparse_kernel,
+                                                                  kSpWarps * 32, smem));
+    const int64_t grid = std::min<int64_t>(ceil_div(P.ntiles, kSpWarps),
+                                           (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
     call.before_launch("mttkrp_sparse");
-    mttkrp_sparse_kernel<<<(unsigned)P.ntiles, kSpWarps * 32, smem, call.stream()>>>(P);
+    mttkrp_sparse_kernel<<<(unsigned)grid, kSpWarps * 32, smem, call.stream()>>>(P);
     call.after_launch();
     const int64_t nnz = call.read_scalar(P.total_nnz);
     call.finish_csr_result(A, nnz);
