@@ -7,25 +7,29 @@
 // (Workspace::insert / drain, workspace.cpp:34-71).
 //
 // B200 design: symbolic pass -> scan -> numeric pass.
-//  * rowprod: products per row P_i = sum_{k in A_i} nnz(B_k) (also the
-//    binning key), and per-bin row lists.
+//  * rowprod (one pass over A): products per row P_i = sum_{k in A_i} nnz(B_k)
+//    (the binning key), and for every A entry its B-row start and its
+//    row-local product offset, so every later kernel maps product j of a row
+//    to (A entry, B position) with no staging and no block barriers.
 //  * bins by P_i (exact output upper bound):
-//      tiny   P <= 32   : warp per row, one product per lane; distinct rank by
-//                         a shuffle sweep, values summed in canonical order
-//                         (bit-exact with the reference).
-//      hash-S P <= 256  : one-warp CTA per row,
-//      hash-M P <= 1024 : 128-thread CTA per row,
-//      hash-L P <= 4096 : 256-thread CTA per row — a shared-memory hash table
-//                         whose hash is ORDER-PRESERVING (slot = scaled column,
-//                         linear probing forward, no wrap): occupied runs are
-//                         mutually ordered, so sorting the few entries of each
-//                         run gives the sorted row; values accumulate with
-//                         shared-memory fp64 atomics.
-//      long   P > 4096  : 512-thread CTA per row, a column bitmap over all
-//                         columns in shared memory (popcount rank) and fp64
-//                         atomics into the pre-assembled output row.
-//  * products are enumerated flattened (prefix of B-row lengths over the A
-//    row), warp-contiguous and lane-interleaved, so B rows are read coalesced.
+//      tiny8/16/32 P <= 8/16/32 : groups of 8/16/32 lanes per row (4/2/1 rows
+//                                 per warp), one product per lane; distinct
+//                                 rank by a shuffle sweep, values summed in
+//                                 canonical order (bit-exact with the CPU).
+//      hash XS/S/M/L P <= 64/256/1024/4096 : CTA of 1/2/8/32 warps per row with a
+//                                 shared-memory hash table sized 2P whose hash
+//                                 is ORDER-PRESERVING (slot = scaled column,
+//                                 forward linear probing, no wrap): occupied
+//                                 runs are mutually ordered, so sorting the
+//                                 few entries of each run gives the sorted row;
+//                                 values accumulate with shared fp64 atomics.
+//      long P > 4096          : 1024-thread CTA per row (rows claimed longest
+//                                 first), a column bitmap over all columns in
+//                                 shared memory (popcount rank) and fp64
+//                                 atomics into the pre-assembled output row.
+//  * products are enumerated flattened, warp-contiguous and lane-interleaved
+//    (B rows read coalesced), with 4 independent gathers in flight per lane.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
@@ -38,19 +42,31 @@
 namespace stamgpu {
 namespace {
 
-enum Bin : int { kBinEmpty = 0, kBinTiny, kBinHashXS, kBinHashS, kBinHashM, kBinHashL, kBinLong, kNumBins };
-constexpr int64_t kTinyMax = 32, kHashXSMax = 64, kHashSMax = 256, kHashMMax = 1024, kHashLMax = 4096;
-constexpr int kAChunk = 1024;        // A entries staged per chunk (long rows)
-constexpr int kLongThreads = 512;
+enum Bin : int {
+  kBinEmpty = 0,
+  kBinTiny8,
+  kBinTiny16,
+  kBinTiny32,
+  kBinHashXS,
+  kBinHashS,
+  kBinHashM,
+  kBinHashL,
+  kBinLong,
+  kNumBins
+};
+constexpr int kLongThreads = 1024;
 constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr int kBatch = 4;  // independent product gathers in flight per lane
 
 __host__ __device__ inline int bin_of(int64_t p) {
   if (p == 0) return kBinEmpty;
-  if (p <= kTinyMax) return kBinTiny;
-  if (p <= kHashXSMax) return kBinHashXS;
-  if (p <= kHashSMax) return kBinHashS;
-  if (p <= kHashMMax) return kBinHashM;
-  if (p <= kHashLMax) return kBinHashL;
+  if (p <= 8) return kBinTiny8;
+  if (p <= 16) return kBinTiny16;
+  if (p <= 32) return kBinTiny32;
+  if (p <= 64) return kBinHashXS;
+  if (p <= 256) return kBinHashS;
+  if (p <= 1024) return kBinHashM;
+  if (p <= 4096) return kBinHashL;
   return kBinLong;
 }
 
@@ -63,162 +79,189 @@ struct SpgemmParams {
   const int64_t* bidx;
   const double* bvals;
   int64_t* prod;             // [m] products per row
+  int* aoff;                 // [nnz(A)] row-local product offset of each A entry
+  int64_t* bst;              // [nnz(A)] start of the entry's B row
   unsigned long long* bins;  // [kNumBins] counts, then cursors
   int64_t* bin_rows;         // [m] rows grouped by bin
   int64_t* cpos;             // [m+1]: counts at [i+1], then offsets
   int64_t* cidx;
   double* cvals;
-  int64_t* stats;            // [0] total products
+  int64_t* stats;            // [0] total products, [1] max products of a row
 };
 
 // ---------------------------------------------------------------------------
+// rowprod: lane per row (32 rows in flight per warp); rows with more than 64
+// A entries are walked cooperatively by the warp.
 __global__ void rowprod_kernel(const SpgemmParams P) {
   __shared__ unsigned long long hist[kNumBins];
-  __shared__ unsigned long long total;
+  __shared__ unsigned long long total, maxp;
   if (threadIdx.x < kNumBins) hist[threadIdx.x] = 0;
-  if (threadIdx.x == 0) total = 0;
+  if (threadIdx.x == 0) total = maxp = 0;
   __syncthreads();
-  // 8 lanes per row, 4 rows in flight per warp
   const unsigned lane = lane_id();
-  const unsigned sub = lane & 7;
-  const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) >> 3;
-  const int64_t iters = (P.m + ngroups - 1) / ngroups;
-  unsigned long long local_total = 0;
-  for (int64_t it = 0; it < iters; it++) {
-    const int64_t i = group + it * ngroups;
-    int64_t s = 0;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long local_total = 0, local_max = 0;
+  for (int64_t base = warp * 32; base < P.m; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    int64_t s = 0, a0 = 0, a1 = 0;
     if (i < P.m) {
-      const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
-      for (int64_t p = a0 + sub; p < a1; p += 8) {
+      a0 = P.apos[i];
+      a1 = P.apos[i + 1];
+    }
+    const bool longrow = a1 - a0 > 64;
+    if (!longrow) {
+#pragma unroll 4
+      for (int64_t p = a0; p < a1; p++) {
         const int64_t k = P.aidx[p];
-        s += P.bpos[k + 1] - P.bpos[k];
+        const int64_t b0 = P.bpos[k];
+        P.bst[p] = b0;
+        P.aoff[p] = (int)s;
+        s += P.bpos[k + 1] - b0;
       }
     }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    if (sub == 0 && i < P.m) {
+    unsigned pending = __ballot_sync(kFull, longrow);
+    while (pending) {
+      const int src = __ffs(pending) - 1;
+      pending &= pending - 1;
+      const int64_t b0 = __shfl_sync(kFull, a0, src), b1 = __shfl_sync(kFull, a1, src);
+      int64_t carry = 0;
+      for (int64_t c = b0; c < b1; c += 32) {
+        const int64_t p = c + lane;
+        int64_t len = 0;
+        if (p < b1) {
+          const int64_t k = P.aidx[p];
+          const int64_t bs = P.bpos[k];
+          len = P.bpos[k + 1] - bs;
+          P.bst[p] = bs;
+        }
+        const int64_t inc = warp_inclusive_scan(len);
+        if (p < b1) P.aoff[p] = (int)(carry + inc - len);
+        carry += __shfl_sync(kFull, inc, 31);
+      }
+      if ((int)lane == src) s = carry;
+    }
+    if (i < P.m) {
       P.prod[i] = s;
       atomicAdd(&hist[bin_of(s)], 1ull);
       local_total += (unsigned long long)s;
+      local_max = max(local_max, (unsigned long long)s);
     }
   }
   local_total = warp_sum(local_total);
-  if (lane == 0 && local_total) atomicAdd(&total, local_total);
+  local_max = warp_max(local_max);
+  if (lane == 0) {
+    if (local_total) atomicAdd(&total, local_total);
+    atomicMax(&maxp, local_max);
+  }
   __syncthreads();
   if (threadIdx.x < kNumBins && hist[threadIdx.x]) atomicAdd(&P.bins[threadIdx.x], hist[threadIdx.x]);
-  if (threadIdx.x == 0 && total) atomicAdd((unsigned long long*)&P.stats[0], total);
+  if (threadIdx.x == 0) {
+    if (total) atomicAdd((unsigned long long*)&P.stats[0], total);
+    atomicMax((unsigned long long*)&P.stats[1], maxp);
+  }
 }
 
 __global__ void bin_scatter_kernel(const SpgemmParams P, const unsigned long long* offsets) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < P.m;
   const int b = valid ? bin_of(P.prod[i]) : -1;
-  // warp-aggregated slot claims
   const unsigned peers = __match_any_sync(kFull, b);
   const int leader = __ffs(peers) - 1;
   unsigned long long base = 0;
   if ((int)lane_id() == leader && valid && b != kBinEmpty)
     base = atomicAdd(&P.bins[b], (unsigned long long)__popc(peers));
   base = __shfl_sync(kFull, base, leader);
-  if (valid && b != kBinEmpty) {
-    const unsigned rank = __popc(peers & lanemask_lt());
-    P.bin_rows[offsets[b] + base + rank] = i;
+  if (valid && b != kBinEmpty) P.bin_rows[offsets[b] + base + __popc(peers & lanemask_lt())] = i;
+}
+
+// A entry of row [a0, a0+na) holding product j: last p with aoff[a0+p] <= j.
+__device__ __forceinline__ int entry_of(const int* aoff, int na, int j) {
+  int lo = 0, hi = na;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (aoff[mid] <= j) lo = mid; else hi = mid;
   }
+  return lo;
 }
 
 // ---------------------------------------------------------------------------
-// tiny rows: one product per lane (P <= 32)
-// Enumerates row i's products into lanes in canonical order.
-__device__ __forceinline__ void tiny_products(const SpgemmParams& P, int64_t i, int64_t& col,
-                                              double& val, bool& has) {
-  const unsigned lane = lane_id();
-  const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
+// tiny rows: groups of G lanes per row, one product per lane (P <= G)
+template <int G>
+__device__ __forceinline__ void tiny_product(const SpgemmParams& P, int64_t i, bool valid, int g,
+                                             bool numeric, int64_t& col, double& val, bool& has) {
   has = false;
   col = INT64_MAX;
   val = 0.0;
-  int64_t done = 0;  // products emitted before this chunk of A entries
-  for (int64_t c = a0; c < a1; c += 32) {
-    const int64_t p = c + lane;
-    int64_t b0 = 0, len = 0;
-    double a = 0.0;
-    if (p < a1) {
-      const int64_t k = P.aidx[p];
-      b0 = P.bpos[k];
-      len = P.bpos[k + 1] - b0;
-      a = P.avals[p];
-    }
-    const int64_t inc = warp_inclusive_scan(len);
-    const int64_t exc = inc - len;
-    const int64_t total = __shfl_sync(kFull, inc, 31);
-    // product j (= lane - done) comes from the A entry whose range holds it
-    const int64_t j = (int64_t)lane - done;
-    int src = 0;
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      const int cand = src + s;
-      const int64_t e = __shfl_sync(kFull, exc, cand & 31);
-      if (cand < 32 && e <= j) src = cand;
-    }
-    const int64_t sb0 = __shfl_sync(kFull, b0, src);
-    const int64_t sexc = __shfl_sync(kFull, exc, src);
-    const double sa = __shfl_sync(kFull, a, src);
-    if (j >= 0 && j < total) {
-      const int64_t q = sb0 + (j - sexc);
-      col = P.bidx[q];
-      val = mul_rn(sa, P.bvals[q]);
-      has = true;
-    }
-    done += total;
-  }
+  if (!valid) return;
+  const int64_t a0 = P.apos[i];
+  const int na = (int)(P.apos[i + 1] - a0);
+  const int prod = (int)P.prod[i];
+  if (g >= prod) return;
+  const int p = entry_of(P.aoff + a0, na, g);
+  const int64_t q = P.bst[a0 + p] + (g - P.aoff[a0 + p]);
+  col = P.bidx[q];
+  if (numeric) val = mul_rn(P.avals[a0 + p], P.bvals[q]);
+  has = true;
 }
 
+template <int G>
 __global__ void tiny_symbolic_kernel(const SpgemmParams P, const int64_t* rows, int64_t nrows) {
-  const unsigned lane = lane_id();
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < nrows; r += nwarps) {
-    const int64_t i = rows[r];
+  const int lane = (int)lane_id();
+  const int g = lane % G;
+  const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int64_t iters = (nrows + ngroups - 1) / ngroups;
+  for (int64_t it = 0; it < iters; it++) {
+    const int64_t r = group + it * ngroups;
+    const bool valid = r < nrows;
+    const int64_t i = valid ? rows[r] : 0;
     int64_t col;
     double val;
     bool has;
-    tiny_products(P, i, col, val, has);
-    // leader: no lower lane holds the same column
+    tiny_product<G>(P, i, valid, g, false, col, val, has);
     bool lead = has;
-    for (int j = 0; j < 32; j++) {
-      const int64_t cj = __shfl_sync(kFull, col, j);
-      if (j < (int)lane && cj == col) lead = false;
+#pragma unroll
+    for (int t = 0; t < G; t++) {
+      const int64_t ct = __shfl_sync(kFull, col, t, G);
+      if (t < g && ct == col) lead = false;
     }
-    const int cnt = __popc(__ballot_sync(kFull, lead));
-    if (lane == 0) P.cpos[i + 1] = cnt;
+    const unsigned m = __ballot_sync(kFull, lead);
+    const unsigned gm = (G == 32) ? kFull : (((1u << G) - 1u) << (lane - g));
+    if (valid && g == 0) P.cpos[i + 1] = __popc(m & gm);
   }
 }
 
+template <int G>
 __global__ void tiny_numeric_kernel(const SpgemmParams P, const int64_t* rows, int64_t nrows) {
-  const unsigned lane = lane_id();
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < nrows; r += nwarps) {
-    const int64_t i = rows[r];
+  const int lane = (int)lane_id();
+  const int g = lane % G;
+  const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int64_t iters = (nrows + ngroups - 1) / ngroups;
+  for (int64_t it = 0; it < iters; it++) {
+    const int64_t r = group + it * ngroups;
+    const bool valid = r < nrows;
+    const int64_t i = valid ? rows[r] : 0;
     int64_t col;
     double val;
     bool has;
-    tiny_products(P, i, col, val, has);
+    tiny_product<G>(P, i, valid, g, true, col, val, has);
     bool lead = has;
+#pragma unroll
+    for (int t = 0; t < G; t++) {
+      const int64_t ct = __shfl_sync(kFull, col, t, G);
+      if (t < g && ct == col) lead = false;
+    }
+    const unsigned lead_mask = __ballot_sync(kFull, lead) >> (lane - g);
     int out = 0;
     double w = add_rn(0.0, val);  // first insert accumulates into 0.0
-    // pass 1: leader flags
-    for (int j = 0; j < 32; j++) {
-      const int64_t cj = __shfl_sync(kFull, col, j);
-      if (j < (int)lane && cj == col) lead = false;
-    }
-    const unsigned lead_mask = __ballot_sync(kFull, lead);
-    // pass 2: slot = leaders with a smaller column; sum later equal products
-    for (int j = 0; j < 32; j++) {
-      const int64_t cj = __shfl_sync(kFull, col, j);
-      const double vj = __shfl_sync(kFull, val, j);
-      if (((lead_mask >> j) & 1u) && cj < col) out++;
-      if (j > (int)lane && cj == col) w = add_rn(w, vj);
+#pragma unroll
+    for (int t = 0; t < G; t++) {
+      const int64_t ct = __shfl_sync(kFull, col, t, G);
+      const double vt = __shfl_sync(kFull, val, t, G);
+      if (((lead_mask >> t) & 1u) && ct < col) out++;
+      if (t > g && ct == col) w = add_rn(w, vt);
     }
     if (lead) {
       const int64_t dst = P.cpos[i] + out;
@@ -229,67 +272,52 @@ __global__ void tiny_numeric_kernel(const SpgemmParams P, const int64_t* rows, i
 }
 
 // ---------------------------------------------------------------------------
-// Flattened product enumeration for CTA-per-row kernels.
-//
-// A chunk of up to kAChunk A entries of row i is staged in smem (B row start,
-// A value, exclusive prefix of B row lengths).  Products [0, total) of the
-// chunk are split into warp-contiguous ranges, lane-interleaved inside them.
-template <int AC>
-struct ChunkSmem {
-  int64_t bstart[AC];
-  double aval[AC];
-  int off[AC + 1];
-  int scan[33];
-};
-
-// Stages A entries [c0, c1) (c1 - c0 <= AC); returns the product total.
-template <int AC>
-__device__ int stage_chunk(const SpgemmParams& P, ChunkSmem<AC>& S, int64_t c0, int64_t c1) {
-  const int n = (int)(c1 - c0);
-  int carry = 0;
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int t = base + threadIdx.x;
-    int len = 0;
-    if (t < n) {
-      const int64_t k = P.aidx[c0 + t];
-      const int64_t b0 = P.bpos[k];
-      len = (int)(P.bpos[k + 1] - b0);
-      S.bstart[t] = b0;
-      S.aval[t] = P.avals[c0 + t];
-    }
-    int tot;
-    const int exc = block_exclusive_scan(len, S.scan, &tot);
-    if (t < n) S.off[t] = carry + exc;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) S.off[n] = carry;
-  __syncthreads();
-  return carry;
-}
-
-// Calls f(col, value) for every product of the staged chunk, each exactly once.
-template <int AC, typename F>
-__device__ __forceinline__ void for_products(const SpgemmParams& P, const ChunkSmem<AC>& S, int nA,
-                                             int total, F f) {
+// Flattened product enumeration for CTA-per-row kernels: the row's products
+// [0, P_i) are split into warp-contiguous ranges, lane-interleaved inside
+// them; each lane keeps its own A-entry cursor and issues kBatch independent
+// (idx, val) gathers before consuming them.  f(col, value) sees every product
+// exactly once; kNumeric false skips the value loads.
+template <bool kNumeric, typename F>
+__device__ __forceinline__ void for_products(const SpgemmParams& P, int64_t a0, int na, int total,
+                                             F f) {
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int per = (total + nwarps - 1) / nwarps;
   const int w0 = min(total, warp * per), w1 = min(total, w0 + per);
-  // A entry holding product w0 (binary search), then advance monotonically
-  int p = 0;
-  {
-    int lo = 0, hi = nA;  // last p with off[p] <= w0
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (S.off[mid] <= w0) lo = mid; else hi = mid;
+  if (w0 >= w1) return;
+  const int* aoff = P.aoff + a0;
+  int p = entry_of(aoff, na, w0);
+  for (int base = w0; base < w1; base += 32 * kBatch) {
+    int64_t q[kBatch];
+    double av[kBatch];
+    bool ok[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) {
+      const int j = base + 32 * u + lane;
+      ok[u] = j < w1;
+      q[u] = 0;
+      av[u] = 0.0;
+      if (ok[u]) {
+        while (p + 1 < na && aoff[p + 1] <= j) p++;
+        q[u] = P.bst[a0 + p] + (j - aoff[p]);
+        if (kNumeric) av[u] = P.avals[a0 + p];
+      }
     }
-    p = lo;
-  }
-  for (int j = w0 + lane; j < w1; j += 32) {
-    while (S.off[p + 1] <= j) p++;
-    const int64_t q = S.bstart[p] + (j - S.off[p]);
-    f(P.bidx[q], mul_rn(S.aval[p], P.bvals[q]));
+    int64_t col[kBatch];
+    double bv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; u++) {
+      col[u] = 0;
+      bv[u] = 0.0;
+      if (ok[u]) {
+        col[u] = P.bidx[q[u]];
+        if (kNumeric) bv[u] = P.bvals[q[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; u++)
+      if (ok[u]) f(col[u], kNumeric ? mul_rn(av[u], bv[u]) : 0.0);
   }
 }
 
@@ -303,43 +331,47 @@ struct SlotMap {
 };
 
 // Column span of row i from the first/last column of every B row it touches.
-__device__ SlotMap row_slot_map(const SpgemmParams& P, int64_t i, int tb, int64_t* red) {
+__device__ SlotMap row_slot_map(const SpgemmParams& P, int64_t a0, int na, int total, int tb,
+                                int64_t* red) {
   int64_t lo = INT64_MAX, hi = -1;
-  const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
-  for (int64_t p = a0 + threadIdx.x; p < a1; p += blockDim.x) {
-    const int64_t k = P.aidx[p];
-    const int64_t b0 = P.bpos[k], b1 = P.bpos[k + 1];
-    if (b1 > b0) {
+  for (int p = threadIdx.x; p < na; p += blockDim.x) {
+    const int o = P.aoff[a0 + p];
+    const int e = (p + 1 < na) ? P.aoff[a0 + p + 1] : total;
+    if (e > o) {
+      const int64_t b0 = P.bst[a0 + p];
       lo = min(lo, P.bidx[b0]);
-      hi = max(hi, P.bidx[b1 - 1]);
+      hi = max(hi, P.bidx[b0 + (e - o) - 1]);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = min(lo, __shfl_xor_sync(kFull, lo, o));
-    hi = max(hi, __shfl_xor_sync(kFull, hi, o));
+  lo = -warp_max(-lo);
+  hi = warp_max(hi);
+  if (blockDim.x == 32) {
+    if (threadIdx.x == 0) {
+      red[0] = lo;
+      red[1] = hi;
+    }
+    __syncwarp();
+  } else {
+    if (threadIdx.x == 0) {
+      red[0] = INT64_MAX;
+      red[1] = -1;
+    }
+    __syncthreads();
+    if (lane_id() == 0) {
+      atomicMin((long long*)&red[0], (long long)lo);
+      atomicMax((long long*)&red[1], (long long)hi);
+    }
+    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    red[0] = INT64_MAX;
-    red[1] = -1;
-  }
-  __syncthreads();
-  if (lane_id() == 0) {
-    atomicMin((long long*)&red[0], (long long)lo);
-    atomicMax((long long*)&red[1], (long long)hi);
-  }
-  __syncthreads();
   SlotMap sm;
   sm.c0 = red[0];
   const uint64_t span = red[1] >= red[0] ? (uint64_t)(red[1] - red[0] + 1) : 1;
   sm.scale = ((uint64_t)tb << 32) / span;
   if (sm.scale == 0) sm.scale = 1;
-  __syncthreads();
   return sm;
 }
 
 // Insert col (linear probing forward from its order-preserving slot).
-// Returns the slot and whether this call created the entry.
 __device__ __forceinline__ int hash_insert(uint32_t* keys, uint32_t key, int slot, bool& created) {
   while (true) {
     const uint32_t old = atomicCAS(&keys[slot], kEmpty, key);
@@ -355,22 +387,16 @@ __device__ __forceinline__ int hash_insert(uint32_t* keys, uint32_t key, int slo
   }
 }
 
-// Table layout for the hash kernels: up to TB main slots + TB/2 overflow
-// slots.  A row with P products uses tb = next_pow2(2P) main slots (at least
-// 64) and tb/2 overflow slots: at most P <= tb/2 entries are inserted, so
-// forward probing never runs off the end.
-// A entries staged per chunk: a row of a hash bin has at most TB/2 products,
-// hence at most TB/2 non-empty A entries; empty ones cost extra chunks only.
-template <int TB>
-constexpr int hash_achunk() { return TB / 2 < kAChunk ? TB / 2 : kAChunk; }
-
+// A row with P products uses tb = next_pow2(2P) main slots (at least 64) and
+// tb/2 overflow slots: at most P <= tb/2 entries are inserted, so forward
+// probing never runs off the end.
 template <int TB>
 struct HashSmem {
-  ChunkSmem<hash_achunk<TB>()> chunk;
   uint32_t keys[TB + TB / 2];
   double vals[TB + TB / 2];
   int64_t red[2];
   int scan[33];
+  int64_t claimed;
 };
 
 __device__ __forceinline__ int row_table(int64_t prod) {
@@ -379,8 +405,6 @@ __device__ __forceinline__ int row_table(int64_t prod) {
   return tb;
 }
 
-// Exclusive scan of one flag per thread across the CTA (warp-only CTAs use a
-// ballot), returning the total through *tot.
 template <int THREADS>
 __device__ __forceinline__ int cta_flag_scan(bool f, int* sh, int* tot) {
   if constexpr (THREADS == 32) {
@@ -397,73 +421,92 @@ __device__ __forceinline__ void cta_sync() {
   if constexpr (THREADS == 32) __syncwarp(); else __syncthreads();
 }
 
+template <int THREADS>
+__device__ __forceinline__ int64_t claim_row(unsigned long long* claim, int64_t* sh) {
+  if (threadIdx.x == 0) *sh = (int64_t)atomicAdd(claim, 1ull);
+  cta_sync<THREADS>();
+  const int64_t r = *sh;
+  cta_sync<THREADS>();
+  return r;
+}
+
+template <int THREADS>
+__device__ __forceinline__ int cta_sum(int v, int* sh) {
+  if constexpr (THREADS == 32) {
+    return warp_sum(v);
+  } else {
+    int tot;
+    block_exclusive_scan(v, sh, &tot);
+    return tot;
+  }
+}
+
 template <int THREADS, int TB>
 __global__ void __launch_bounds__(THREADS) hash_symbolic_kernel(const SpgemmParams P,
                                                                  const int64_t* rows,
-                                                                 int64_t nrows) {
+                                                                 int64_t nrows,
+                                                                 unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   HashSmem<TB>& S = *reinterpret_cast<HashSmem<TB>*>(smem_raw);
-  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+  while (true) {
+    const int64_t r = claim_row<THREADS>(claim, &S.claimed);
+    if (r >= nrows) break;
     const int64_t i = rows[r];
-    const int tb = row_table(P.prod[i]);
+    const int total = (int)P.prod[i];
+    const int tb = row_table(total);
     const int nslots = tb + tb / 2;
-    const SlotMap sm = row_slot_map(P, i, tb, S.red);
+    const int64_t a0 = P.apos[i];
+    const int na = (int)(P.apos[i + 1] - a0);
+    const SlotMap sm = row_slot_map(P, a0, na, total, tb, S.red);
     for (int s = threadIdx.x; s < nslots; s += THREADS) S.keys[s] = kEmpty;
-    __syncthreads();
-    const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
+    cta_sync<THREADS>();
     int created = 0;
-    constexpr int AC = hash_achunk<TB>();
-    for (int64_t c0 = a0; c0 < a1; c0 += AC) {
-      const int64_t c1 = min(a1, c0 + AC);
-      const int total = stage_chunk(P, S.chunk, c0, c1);
-      for_products(P, S.chunk, (int)(c1 - c0), total, [&](int64_t col, double) {
-        bool made;
-        hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
-        created += made ? 1 : 0;
-      });
-      __syncthreads();
-    }
-    int tot;
-    block_exclusive_scan(created, S.scan, &tot);
+    for_products<false>(P, a0, na, total, [&](int64_t col, double) {
+      bool made;
+      hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
+      created += made ? 1 : 0;
+    });
+    const int tot = cta_sum<THREADS>(created, S.scan);
     if (threadIdx.x == 0) P.cpos[i + 1] = tot;
+    cta_sync<THREADS>();
   }
 }
 
 template <int THREADS, int TB>
 __global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParams P,
                                                                 const int64_t* rows,
-                                                                int64_t nrows) {
+                                                                int64_t nrows,
+                                                                unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   HashSmem<TB>& S = *reinterpret_cast<HashSmem<TB>*>(smem_raw);
-  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+  while (true) {
+    const int64_t r = claim_row<THREADS>(claim, &S.claimed);
+    if (r >= nrows) break;
     const int64_t i = rows[r];
-    const int tb = row_table(P.prod[i]);
+    const int total = (int)P.prod[i];
+    const int tb = row_table(total);
     const int nslots = tb + tb / 2;
-    const SlotMap sm = row_slot_map(P, i, tb, S.red);
+    const int64_t a0 = P.apos[i];
+    const int na = (int)(P.apos[i + 1] - a0);
+    const SlotMap sm = row_slot_map(P, a0, na, total, tb, S.red);
     for (int s = threadIdx.x; s < nslots; s += THREADS) {
       S.keys[s] = kEmpty;
       S.vals[s] = 0.0;
     }
-    __syncthreads();
-    const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
-    constexpr int AC = hash_achunk<TB>();
-    for (int64_t c0 = a0; c0 < a1; c0 += AC) {
-      const int64_t c1 = min(a1, c0 + AC);
-      const int total = stage_chunk(P, S.chunk, c0, c1);
-      for_products(P, S.chunk, (int)(c1 - c0), total, [&](int64_t col, double v) {
-        bool made;
-        const int s = hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
-        atomicAdd(&S.vals[s], v);
-      });
-      __syncthreads();
-    }
-    // sort every occupied run (runs are mutually ordered), started by the
-    // thread that owns the run's first slot
+    cta_sync<THREADS>();
+    for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
+      bool made;
+      const int s = hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
+      atomicAdd(&S.vals[s], v);
+    });
+    cta_sync<THREADS>();
+    // sort every occupied run (runs are mutually ordered), by the thread that
+    // owns the run's first slot
     for (int s = threadIdx.x; s < nslots; s += THREADS) {
       if (S.keys[s] == kEmpty || (s > 0 && S.keys[s - 1] != kEmpty)) continue;
       int e = s + 1;
       while (e < nslots && S.keys[e] != kEmpty) e++;
-      for (int a = s + 1; a < e; a++) {  // insertion sort of the run
+      for (int a = s + 1; a < e; a++) {
         const uint32_t k = S.keys[a];
         const double v = S.vals[a];
         int b = a - 1;
@@ -476,7 +519,7 @@ __global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParam
         S.vals[b + 1] = v;
       }
     }
-    __syncthreads();
+    cta_sync<THREADS>();
     // compact occupied slots in order, straight to the output row
     const int64_t dst = P.cpos[i];
     int64_t written = 0;
@@ -491,19 +534,19 @@ __global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParam
       }
       written += tot;
     }
-    __syncthreads();
+    cta_sync<THREADS>();
   }
 }
 
 // ---------------------------------------------------------------------------
 // Long rows: a bitmap over all n columns in shared memory (64-bit words), and
 // for the numeric pass an exclusive popcount prefix per word.
-struct LongSmem {
-  ChunkSmem<kAChunk> chunk;
+struct LongHeader {
   int scan[33];
+  int64_t claimed;
 };
 
-__host__ __device__ inline size_t long_header() { return (sizeof(LongSmem) + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t long_header() { return (sizeof(LongHeader) + 15) & ~(size_t)15; }
 
 __host__ __device__ inline size_t long_smem_bytes(int64_t n, bool numeric) {
   const size_t nw = (size_t)((n + 63) / 64);
@@ -516,23 +559,22 @@ __device__ __forceinline__ void set_bit(unsigned long long* bits, int64_t col) {
 
 __global__ void __launch_bounds__(kLongThreads) long_symbolic_kernel(const SpgemmParams P,
                                                                      const int64_t* rows,
-                                                                     int64_t nrows) {
+                                                                     int64_t nrows,
+                                                                     unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LongSmem& S = *reinterpret_cast<LongSmem*>(smem_raw);
+  LongHeader& S = *reinterpret_cast<LongHeader*>(smem_raw);
   auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
   const int nw = (int)((P.n + 63) >> 6);
-  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+  while (true) {
+    const int64_t r = claim_row<kLongThreads>(claim, &S.claimed);
+    if (r >= nrows) break;
     const int64_t i = rows[r];
     for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
     __syncthreads();
-    const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
-    for (int64_t c0 = a0; c0 < a1; c0 += kAChunk) {
-      const int64_t c1 = min(a1, c0 + kAChunk);
-      const int total = stage_chunk(P, S.chunk, c0, c1);
-      for_products(P, S.chunk, (int)(c1 - c0), total,
-                   [&](int64_t col, double) { set_bit(bits, col); });
-      __syncthreads();
-    }
+    const int64_t a0 = P.apos[i];
+    for_products<false>(P, a0, (int)(P.apos[i + 1] - a0), (int)P.prod[i],
+                        [&](int64_t col, double) { set_bit(bits, col); });
+    __syncthreads();
     int cnt = 0;
     for (int w = threadIdx.x; w < nw; w += blockDim.x) cnt += __popcll(bits[w]);
     int tot;
@@ -543,28 +585,28 @@ __global__ void __launch_bounds__(kLongThreads) long_symbolic_kernel(const Spgem
 
 __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const SpgemmParams P,
                                                                     const int64_t* rows,
-                                                                    int64_t nrows) {
+                                                                    int64_t nrows,
+                                                                    unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LongSmem& S = *reinterpret_cast<LongSmem*>(smem_raw);
+  LongHeader& S = *reinterpret_cast<LongHeader*>(smem_raw);
   auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
   const int nw = (int)((P.n + 63) >> 6);
   int* wpre = reinterpret_cast<int*>(bits + nw);
   const int per = (nw + kLongThreads - 1) / kLongThreads;  // words per thread
-  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+  while (true) {
+    const int64_t r = claim_row<kLongThreads>(claim, &S.claimed);
+    if (r >= nrows) break;
     const int64_t i = rows[r];
     const int64_t dst = P.cpos[i];
     const int64_t cnt = P.cpos[i + 1] - dst;
     for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
     for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) P.cvals[dst + t] = 0.0;
     __syncthreads();
-    const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
-    for (int64_t c0 = a0; c0 < a1; c0 += kAChunk) {
-      const int64_t c1 = min(a1, c0 + kAChunk);
-      const int total = stage_chunk(P, S.chunk, c0, c1);
-      for_products(P, S.chunk, (int)(c1 - c0), total,
-                   [&](int64_t col, double) { set_bit(bits, col); });
-      __syncthreads();
-    }
+    const int64_t a0 = P.apos[i];
+    const int na = (int)(P.apos[i + 1] - a0);
+    const int total = (int)P.prod[i];
+    for_products<false>(P, a0, na, total, [&](int64_t col, double) { set_bit(bits, col); });
+    __syncthreads();
     // exclusive popcount prefix per word; write the sorted column list
     const int w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
     int mine = 0;
@@ -582,45 +624,63 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
       }
     }
     __syncthreads();
-    for (int64_t c0 = a0; c0 < a1; c0 += kAChunk) {
-      const int64_t c1 = min(a1, c0 + kAChunk);
-      const int total = stage_chunk(P, S.chunk, c0, c1);
-      for_products(P, S.chunk, (int)(c1 - c0), total, [&](int64_t col, double v) {
-        const int w = (int)(col >> 6);
-        const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
-        atomicAdd(&P.cvals[dst + slot], v);
-      });
-      __syncthreads();
-    }
+    for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
+      const int w = (int)(col >> 6);
+      const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
+      atomicAdd(&P.cvals[dst + slot], v);
+    });
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
 template <int THREADS, int TB>
 void launch_hash(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
-                 bool numeric, const char* name) {
+                 bool numeric, const char* name, unsigned long long* claim) {
   if (n == 0) return;
   const size_t smem = sizeof(HashSmem<TB>);
   auto kern = numeric ? hash_numeric_kernel<THREADS, TB> : hash_symbolic_kernel<THREADS, TB>;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
   STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
-  const int64_t grid = std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * call.ctx()->num_sms * 4);
+  const int64_t grid = std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
   call.before_launch(name);
-  kern<<<(unsigned)grid, THREADS, smem, call.stream()>>>(P, rows, n);
+  kern<<<(unsigned)grid, THREADS, smem, call.stream()>>>(P, rows, n, claim);
   call.after_launch();
 }
 
 void launch_long(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
-                 bool numeric) {
+                 bool numeric, unsigned long long* claim) {
   if (n == 0) return;
   const size_t smem = long_smem_bytes(P.n, numeric);
   auto kern = numeric ? long_numeric_kernel : long_symbolic_kernel;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = std::min<int64_t>(n, call.ctx()->num_sms);
   call.before_launch(numeric ? "spgemm_long_numeric" : "spgemm_long_symbolic");
-  kern<<<(unsigned)grid, kLongThreads, smem, call.stream()>>>(P, rows, n);
+  kern<<<(unsigned)grid, kLongThreads, smem, call.stream()>>>(P, rows, n, claim);
   call.after_launch();
+}
+
+template <int G>
+void launch_tiny(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
+                 bool numeric) {
+  if (n == 0) return;
+  const int64_t threads = n * G;
+  const unsigned grid =
+      (unsigned)std::min<int64_t>(stamrt::ceil_div(threads, 256), (int64_t)call.ctx()->num_sms * 16);
+  call.before_launch(numeric ? "spgemm_tiny_numeric" : "spgemm_tiny_symbolic");
+  if (numeric)
+    tiny_numeric_kernel<G><<<grid, 256, 0, call.stream()>>>(P, rows, n);
+  else
+    tiny_symbolic_kernel<G><<<grid, 256, 0, call.stream()>>>(P, rows, n);
+  call.after_launch();
+}
+
+// Orders the long rows longest first (greedy LPT over the dynamic claims).
+__global__ void gather_keys_kernel(const int64_t* rows, int64_t n, const int64_t* prod,
+                                   uint64_t* keys) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) keys[t] = (uint64_t)prod[rows[t]];
 }
 
 }  // namespace
@@ -635,14 +695,12 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
     check_csr_view(A, "spgemm A");
     check_csr_view(B, "spgemm B");
-    if (A->ncols != B->nrows)
-      fail(STAM_ERR_DIMENSION_MISMATCH, "spgemm: A columns != B rows");
+    if (A->ncols != B->nrows) fail(STAM_ERR_DIMENSION_MISMATCH, "spgemm: A columns != B rows");
     if (call.opts().mode != STAM_MODE_FUSED)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm supports fused mode only in ABI v1");
     if (B->ncols >= (int64_t)UINT32_MAX)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: B has 2^32 or more columns");
     const int64_t m = A->nrows, n = B->ncols;
-    const size_t long_smem = long_smem_bytes(n, true);
     SpgemmParams P{};
     P.m = m;
     P.n = n;
@@ -653,21 +711,22 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     P.bidx = call.device_input(B->idx, (size_t)B->nnz, B->mem);
     P.bvals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
     P.prod = call.scratch_n<int64_t>((size_t)m);
+    P.aoff = call.scratch_n<int>((size_t)std::max<int64_t>(A->nnz, 1));
+    P.bst = call.scratch_n<int64_t>((size_t)std::max<int64_t>(A->nnz, 1));
     auto* ctl = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * 16));
     P.bins = reinterpret_cast<unsigned long long*>(ctl);
-    P.stats = ctl + 8;
+    P.stats = ctl + kNumBins;
     P.bin_rows = call.scratch_n<int64_t>((size_t)m);
     P.cpos = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * ((size_t)m + 1)));
     const int sms = call.ctx()->num_sms;
 
-    // products per row and bins
     call.before_launch("spgemm_rowprod");
-    rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 32), (int64_t)sms * 8), 256, 0,
+    rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)sms * 8), 256, 0,
                      call.stream()>>>(P);
     call.after_launch();
     int64_t host[16];
+    static_assert(kNumBins + 2 <= 16, "control block");
     call.read_scalars(ctl, 16, host);
-    static_assert(kNumBins <= 8, "bin counters share the control block");
     unsigned long long counts[kNumBins], offsets[kNumBins];
     unsigned long long acc = 0;
     for (int b = 0; b < kNumBins; b++) {
@@ -675,8 +734,10 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
       offsets[b] = acc;
       if (b != kBinEmpty) acc += counts[b];
     }
-    const int64_t products = host[8];
-    if (counts[kBinLong] > 0 && long_smem > call.ctx()->smem_optin)
+    const int64_t products = host[kNumBins], max_prod = host[kNumBins + 1];
+    if (max_prod >= (int64_t)INT32_MAX)
+      fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: a row has 2^31 or more products");
+    if (counts[kBinLong] > 0 && long_smem_bytes(n, true) > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE,
            "spgemm: rows with more than 4096 products need a column bitmap of B's columns in "
            "shared memory (at most ~1.2M columns in ABI v1)");
@@ -690,21 +751,38 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
 
     const int64_t* rows_b[kNumBins];
     for (int b = 0; b < kNumBins; b++) rows_b[b] = P.bin_rows + offsets[b];
-    auto tiny_grid = [&](int64_t n) {
-      return (unsigned)std::min<int64_t>(ceil_div(n, 8), (int64_t)sms * 16);
-    };
-    // symbolic
-    if (counts[kBinTiny]) {
-      call.before_launch("spgemm_tiny_symbolic");
-      tiny_symbolic_kernel<<<tiny_grid(counts[kBinTiny]), 256, 0, call.stream()>>>(
-          P, rows_b[kBinTiny], counts[kBinTiny]);
+    // longest rows first for the long bin
+    if (counts[kBinLong] > 1) {
+      const int64_t nl = (int64_t)counts[kBinLong];
+      auto* keys = call.scratch_n<uint64_t>((size_t)nl * 2);
+      auto* rows_sorted = call.scratch_n<int64_t>((size_t)nl);
+      call.before_launch("spgemm_long_keys");
+      gather_keys_kernel<<<(unsigned)ceil_div(nl, 256), 256, 0, call.stream()>>>(rows_b[kBinLong],
+                                                                                 nl, P.prod, keys);
       call.after_launch();
+      size_t sort_bytes = 0;
+      STAM_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(
+          nullptr, sort_bytes, keys, keys + nl, rows_b[kBinLong], rows_sorted, (int)nl, 0, 40,
+          call.stream()));
+      void* sort_tmp = call.scratch(sort_bytes);
+      call.before_launch("spgemm_long_sort");
+      STAM_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(
+          sort_tmp, sort_bytes, keys, keys + nl, rows_b[kBinLong], rows_sorted, (int)nl, 0, 40,
+          call.stream()));
+      call.after_launch();
+      rows_b[kBinLong] = rows_sorted;
     }
-    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic");
-    launch_hash<32, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic");
-    launch_hash<128, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic");
-    launch_hash<256, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic");
-    launch_long(call, P, rows_b[kBinLong], counts[kBinLong], false);
+    auto* claims = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 16));
+
+    // symbolic
+    launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], false);
+    launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], false);
+    launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], false);
+    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic", claims + 0);
+    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1);
+    launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
+    launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
+    launch_long(call, P, rows_b[kBinLong], counts[kBinLong], false, claims + 4);
 
     // scan counts -> row pointers
     size_t temp_bytes = 0;
@@ -722,17 +800,15 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
                                     cudaMemcpyDeviceToDevice, call.stream()));
     P.cidx = Cr->idx;
     P.cvals = Cr->vals;
-    if (counts[kBinTiny]) {
-      call.before_launch("spgemm_tiny_numeric");
-      tiny_numeric_kernel<<<tiny_grid(counts[kBinTiny]), 256, 0, call.stream()>>>(
-          P, rows_b[kBinTiny], counts[kBinTiny]);
-      call.after_launch();
-    }
-    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric");
-    launch_hash<32, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric");
-    launch_hash<128, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric");
-    launch_hash<256, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric");
-    launch_long(call, P, rows_b[kBinLong], counts[kBinLong], true);
+    // numeric
+    launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], true);
+    launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], true);
+    launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true);
+    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5);
+    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6);
+    launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
+    launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
+    launch_long(call, P, rows_b[kBinLong], counts[kBinLong], true, claims + 9);
 
     call.finish_csr_result(Cr, nnz);
     call.finish();
