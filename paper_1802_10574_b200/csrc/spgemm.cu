@@ -287,20 +287,58 @@ __device__ __forceinline__ void for_products(const SpgemmParams& P, int64_t a0, 
   const int w0 = min(total, warp * per), w1 = min(total, w0 + per);
   if (w0 >= w1) return;
   const int* aoff = P.aoff + a0;
-  int p = entry_of(aoff, na, w0);
+  // pb: A entry holding product `base`; ob: its first product (aoff[pb])
+  int pb = entry_of(aoff, na, w0);
+  int ob = aoff[pb];
+  const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
   for (int base = w0; base < w1; base += 32 * kBatch) {
     int64_t q[kBatch];
     double av[kBatch];
     bool ok[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; u++) {
-      const int j = base + 32 * u + lane;
+      const int wb = base + 32 * u;  // window start (uniform)
+      const int j = wb + lane;
       ok[u] = j < w1;
       q[u] = 0;
       av[u] = 0.0;
+      if (wb >= w1) continue;  // uniform
+      // boundaries of the next 32 entries, relative to the window start
+      const int pe = pb + 1 + lane;
+      const int bnd = pe < na ? aoff[pe] - wb : (1 << 30);
+      const int nxt = __shfl_down_sync(kFull, bnd, 1);
+      const bool empty_seg = lane < 31 && bnd == nxt && bnd <= 32;
+      int p, op;
+      if (!__any_sync(kFull, empty_seg)) {
+        // lane's entry = pb + #boundaries at or below it (all boundaries >= 1)
+        const unsigned M = __reduce_or_sync(kFull, bnd < 32 ? (1u << bnd) : 0u);
+        const int c = __popc(M & upto);
+        p = pb + c;
+        const int bc = __shfl_sync(kFull, bnd, (c + 31) & 31);
+        op = c == 0 ? ob : bc + wb;
+        // advance to the entry holding product wb + 32
+        const int adv = __popc(M) + (__any_sync(kFull, bnd == 32) ? 1 : 0);
+        if (adv > 0) {
+          const int ba = __shfl_sync(kFull, bnd, adv - 1);
+          pb += adv;
+          ob = ba + wb;
+        }
+      } else {
+        // rows with empty B rows in this window: per-lane cursor
+        p = pb;
+        if (ok[u])
+          while (p + 1 < na && aoff[p + 1] <= j) p++;
+        op = aoff[p];
+        const int last = min(wb + 32, total) - 1;
+        int pn = pb;
+        while (pn + 1 < na && aoff[pn + 1] <= last) pn++;
+        // entry holding product wb + 32 (or the last one)
+        while (pn + 1 < na && aoff[pn + 1] <= wb + 32) pn++;
+        pb = __shfl_sync(kFull, pn, 0);
+        ob = aoff[pb];
+      }
       if (ok[u]) {
-        while (p + 1 < na && aoff[p + 1] <= j) p++;
-        q[u] = P.bst[a0 + p] + (j - aoff[p]);
+        q[u] = P.bst[a0 + p] + (j - op);
         if (kNumeric) av[u] = P.avals[a0 + p];
       }
     }
