@@ -50,6 +50,7 @@ enum Bin : int {
   kBinHashXS,
   kBinHashS,
   kBinHashM,
+  kBinHashL1,
   kBinHashL,
   kBinLong,
   kNumBins
@@ -66,6 +67,7 @@ __host__ __device__ inline int bin_of(int64_t p) {
   if (p <= 64) return kBinHashXS;
   if (p <= 256) return kBinHashS;
   if (p <= 1024) return kBinHashM;
+  if (p <= 2048) return kBinHashL1;
   if (p <= 4096) return kBinHashL;
   return kBinLong;
 }
@@ -479,6 +481,83 @@ __device__ __forceinline__ int cta_sum(int v, int* sh) {
   }
 }
 
+// First slot at or after s0 that does not continue an occupied run (a run
+// never crosses it).  Warp-cooperative forward scan; uniform result.
+__device__ __forceinline__ int run_boundary(const uint32_t* keys, int s0, int nslots) {
+  if (s0 <= 0) return 0;
+  if (s0 >= nslots) return nslots;
+  const int lane = (int)lane_id();
+  for (int c = s0; c < nslots; c += 32) {
+    const int s = c + lane;
+    // s is a boundary iff slot s-1 is empty
+    const bool bnd = s >= nslots || keys[s - 1] == kEmpty;
+    const unsigned m = __ballot_sync(kFull, bnd);
+    if (m) return min(nslots, c + __ffs(m) - 1);
+  }
+  return nslots;
+}
+
+// Sorts every occupied run of the table and writes the occupied slots, in
+// slot order, to out_idx/out_vals.  Warps own contiguous slot ranges whose
+// ends sit on run boundaries; one block prefix over the warp counts.
+template <int THREADS>
+__device__ void drain_table(uint32_t* keys, double* vals, int nslots, int64_t c0, int64_t* out_idx,
+                            double* out_vals, int* scan) {
+  constexpr int kWarpsN = THREADS / 32;
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int per = (nslots + kWarpsN - 1) / kWarpsN;
+  const int r0 = run_boundary(keys, warp * per, nslots);
+  const int r1 = run_boundary(keys, (warp + 1) * per, nslots);
+  // sort the runs starting in [r0, r1) (lane per run start)
+  int cnt = 0;
+  for (int c = r0; c < r1; c += 32) {
+    const int s = c + lane;
+    const bool occ = s < r1 && keys[s] != kEmpty;
+    cnt += __popc(__ballot_sync(kFull, occ));
+    if (occ && (s == 0 || keys[s - 1] == kEmpty)) {
+      int e = s + 1;
+      while (e < nslots && keys[e] != kEmpty) e++;
+      for (int a = s + 1; a < e; a++) {
+        const uint32_t k = keys[a];
+        const double v = vals[a];
+        int b = a - 1;
+        while (b >= s && keys[b] > k) {
+          keys[b + 1] = keys[b];
+          vals[b + 1] = vals[b];
+          b--;
+        }
+        keys[b + 1] = k;
+        vals[b + 1] = v;
+      }
+    }
+  }
+  int base = 0;
+  if constexpr (kWarpsN > 1) {
+    if (lane == 0) scan[warp] = cnt;
+    __syncthreads();
+    if (warp == 0) {
+      const int v = lane < kWarpsN ? scan[lane] : 0;
+      const int inc = warp_inclusive_scan(v);
+      if (lane < kWarpsN) scan[lane] = inc - v;
+    }
+    __syncthreads();
+    base = scan[warp];
+  }
+  __syncwarp();
+  for (int c = r0; c < r1; c += 32) {
+    const int s = c + lane;
+    const bool occ = s < r1 && keys[s] != kEmpty;
+    const unsigned m = __ballot_sync(kFull, occ);
+    if (occ) {
+      const int pos = base + __popc(m & lanemask_lt());
+      out_idx[pos] = c0 + (int64_t)keys[s];
+      out_vals[pos] = vals[s];
+    }
+    base += __popc(m);
+  }
+}
+
 template <int THREADS, int TB>
 __global__ void __launch_bounds__(THREADS) hash_symbolic_kernel(const SpgemmParams P,
                                                                  const int64_t* rows,
@@ -521,6 +600,7 @@ __global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParam
     const int64_t r = claim_row<THREADS>(claim, &S.claimed);
     if (r >= nrows) break;
     const int64_t i = rows[r];
+    const int64_t dst = P.cpos[i];  // issued early, used by the drain
     const int total = (int)P.prod[i];
     const int tb = row_table(total);
     const int nslots = tb + tb / 2;
@@ -538,40 +618,8 @@ __global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParam
       atomicAdd(&S.vals[s], v);
     });
     cta_sync<THREADS>();
-    // sort every occupied run (runs are mutually ordered), by the thread that
-    // owns the run's first slot
-    for (int s = threadIdx.x; s < nslots; s += THREADS) {
-      if (S.keys[s] == kEmpty || (s > 0 && S.keys[s - 1] != kEmpty)) continue;
-      int e = s + 1;
-      while (e < nslots && S.keys[e] != kEmpty) e++;
-      for (int a = s + 1; a < e; a++) {
-        const uint32_t k = S.keys[a];
-        const double v = S.vals[a];
-        int b = a - 1;
-        while (b >= s && S.keys[b] > k) {
-          S.keys[b + 1] = S.keys[b];
-          S.vals[b + 1] = S.vals[b];
-          b--;
-        }
-        S.keys[b + 1] = k;
-        S.vals[b + 1] = v;
-      }
-    }
-    cta_sync<THREADS>();
-    // compact occupied slots in order, straight to the output row
-    const int64_t dst = P.cpos[i];
-    int64_t written = 0;
-    for (int c = 0; c < nslots; c += THREADS) {
-      const int s = c + threadIdx.x;
-      const bool occ = s < nslots && S.keys[s] != kEmpty;
-      int tot;
-      const int pos = cta_flag_scan<THREADS>(occ, S.scan, &tot);
-      if (occ) {
-        P.cidx[dst + written + pos] = sm.c0 + (int64_t)S.keys[s];
-        P.cvals[dst + written + pos] = S.vals[s];
-      }
-      written += tot;
-    }
+    // sort the runs (mutually ordered) and write the row in slot order
+    drain_table<THREADS>(S.keys, S.vals, nslots, sm.c0, P.cidx + dst, P.cvals + dst, S.scan);
     cta_sync<THREADS>();
   }
 }
@@ -819,6 +867,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic", claims + 0);
     launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
+    launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], false, "spgemm_hashL1_symbolic", claims + 10);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
     launch_long(call, P, rows_b[kBinLong], counts[kBinLong], false, claims + 4);
 
@@ -845,6 +894,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5);
     launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
+    launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
     launch_long(call, P, rows_b[kBinLong], counts[kBinLong], true, claims + 9);
 
