@@ -678,7 +678,6 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
   auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
   const int nw = (int)((P.n + 63) >> 6);
   int* wpre = reinterpret_cast<int*>(bits + nw);
-  const int per = (nw + kLongThreads - 1) / kLongThreads;  // words per thread
   while (true) {
     const int64_t r = claim_row<kLongThreads>(claim, &S.claimed);
     if (r >= nrows) break;
@@ -693,20 +692,40 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
     const int total = (int)P.prod[i];
     for_products<false>(P, a0, na, total, [&](int64_t col, double) { set_bit(bits, col); });
     __syncthreads();
-    // exclusive popcount prefix per word; write the sorted column list
-    const int w0 = threadIdx.x * per, w1 = min(nw, w0 + per);
-    int mine = 0;
-    for (int w = w0; w < w1; w++) mine += __popcll(bits[w]);
-    int tot;
-    int run = block_exclusive_scan(mine, S.scan, &tot);
-    for (int w = w0; w < w1; w++) {
-      wpre[w] = run;
-      unsigned long long m = bits[w];
-      while (m) {
-        const int b = __ffsll((long long)m) - 1;
-        P.cidx[dst + run] = (int64_t)w * 64 + b;
-        run++;
-        m &= m - 1;
+    // exclusive popcount prefix per word and the sorted column list: warp w
+    // owns words [w*per_w, (w+1)*per_w), lane-interleaved in 32-word chunks
+    {
+      const int lane = (int)lane_id();
+      const int warp = threadIdx.x >> 5;
+      const int per_w = (nw + 31) / 32;
+      const int ww0 = min(nw, warp * per_w), ww1 = min(nw, ww0 + per_w);
+      int mine = 0;
+      for (int w = ww0 + lane; w < ww1; w += 32) mine += __popcll(bits[w]);
+      mine = warp_sum(mine);
+      if (lane == 0) S.scan[warp] = mine;
+      __syncthreads();
+      if (warp == 0) {
+        const int v = S.scan[lane];
+        const int inc = warp_inclusive_scan(v);
+        S.scan[lane] = inc - v;
+      }
+      __syncthreads();
+      int run = S.scan[warp];
+      for (int w = ww0; w < ww1; w += 32) {
+        const int wl = w + lane;
+        const unsigned long long bm = wl < ww1 ? bits[wl] : 0ull;
+        const int c = __popcll(bm);
+        const int inc = warp_inclusive_scan(c);
+        int pos = run + inc - c;
+        if (wl < ww1) wpre[wl] = pos;
+        unsigned long long mm = bm;
+        while (mm) {
+          const int b = __ffsll((long long)mm) - 1;
+          P.cidx[dst + pos] = (int64_t)wl * 64 + b;
+          pos++;
+          mm &= mm - 1;
+        }
+        run += __shfl_sync(kFull, inc, 31);
       }
     }
     __syncthreads();
