@@ -106,9 +106,13 @@ __device__ __forceinline__ int64_t lookback_exclusive(uint64_t* status, int64_t 
     const int64_t t = base - (int64_t)lane;
     uint64_t s = kFlagInc;  // lanes before tile 0 behave like a zero prefix
     if (t >= 0) {
-      do {
-        s = ld_acquire(&status[t]);
-      } while ((s >> 62) == 0);
+      // predecessors still computing: back off so spinning warps do not steal
+      // issue slots from the warps doing the work
+      unsigned ns = 32;
+      while (((s = ld_acquire(&status[t])) >> 62) == 0) {
+        __nanosleep(ns);
+        ns = ns < 2048 ? ns * 2 : ns;
+      }
     }
     const unsigned inc_mask = __ballot_sync(kFull, (s >> 62) == 2);
     // closest predecessor holding an inclusive prefix = lowest set lane
