@@ -388,6 +388,7 @@ struct SparseParams {
   uint64_t* tile_status;
   unsigned long long* tile_counter;
   int64_t* total_nnz;
+  unsigned long long* mults;  // SPEC counter: |D_k| per nonzero + consumed w0 entries
 };
 
 __device__ __forceinline__ int64_t locate(const int64_t* a, int64_t n, int64_t x) {
@@ -410,7 +411,8 @@ __device__ __forceinline__ void ws_add(double* wv, uint32_t* wb, int64_t r, doub
 }
 
 // Evaluates slice i into the warp's workspace (vals[R], bits[R/32]).
-__device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint32_t* wb) {
+__device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint32_t* wb,
+                             unsigned long long& mults) {
   const int lane = (int)lane_id();
   const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
   for (int64_t f = f0 + lane; f < f1; f += 32) {
@@ -424,6 +426,7 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
       const int64_t k = P.idx2[z0];
       const double b = P.vals[z0];
       const int64_t d0 = P.dpos[k], d1 = P.dpos[k + 1];
+      mults += (unsigned long long)(d1 - d0);
       for (int64_t cq = c0; cq < c1; cq += kRowChunk) {
         int cc[kRowChunk];
 #pragma unroll
@@ -441,12 +444,17 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
               // w0(r) = 0 + b*D(k,r);  w1(r) += w0(r)*C(j,r)
               const double w0 = add_rn(0.0, mul_rn(b, P.dvals[dq + hit]));
               ws_add(wv, wb, cc[a], mul_rn(w0, P.cvals[cq + a]));
+              mults++;
             }
           }
         }
       }
     } else {
       // general fiber: w0 at each of C_j's coordinates, accumulated over k
+      for (int64_t z = z0; z < z1; z++) {
+        const int64_t k = P.idx2[z];
+        mults += (unsigned long long)(P.dpos[k + 1] - P.dpos[k]);
+      }
       for (int64_t q = c0; q < c1; q++) {
         const int64_t r = P.cidx[q];
         double w0 = 0.0;
@@ -460,7 +468,10 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
             present = true;
           }
         }
-        if (present) ws_add(wv, wb, r, mul_rn(w0, P.cvals[q]));
+        if (present) {
+          ws_add(wv, wb, r, mul_rn(w0, P.cvals[q]));
+          mults++;
+        }
       }
     }
   }
@@ -476,6 +487,7 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const Spar
   const int nwords = (int)((R + 31) / 32);
   const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
   unsigned char* wbase = smem_raw + (size_t)warp * kSpSlicesPerWarp * ws_bytes;
+  unsigned long long mults = 0;
   while (true) {
     int64_t tile = 0;
     if (lane == 0) tile = (int64_t)atomicAdd(P.tile_counter, 1ull);
@@ -492,7 +504,7 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const Spar
       __syncwarp();
       cnt[k] = 0;
       if (i0 + k < P.I) {
-        sparse_slice(P, i0 + k, wv, wb);
+        sparse_slice(P, i0 + k, wv, wb, mults);
         __syncwarp();
         int64_t c = 0;
         for (int w = lane; w < nwords; w += 32) c += __popc(wb[w]);
@@ -530,6 +542,8 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const Spar
     if (lane == 0 && tile == P.ntiles - 1) *P.total_nnz = base + agg;
     __syncwarp();
   }
+  mults = warp_sum(mults);
+  if (lane == 0 && mults) atomicAdd(P.mults, mults);
 }
 
 }  // namespace
@@ -651,6 +665,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.out_vals = A->vals;
     auto* ctl = static_cast<uint64_t*>(call.scratch_zero((4 + (size_t)P.ntiles) * 8));
     P.tile_counter = reinterpret_cast<unsigned long long*>(ctl);
+    P.mults = reinterpret_cast<unsigned long long*>(ctl + 1);
     P.total_nnz = reinterpret_cast<int64_t*>(ctl + 2);
     P.tile_status = ctl + 4;
     STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_kernel,
@@ -663,10 +678,14 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     call.before_launch("mttkrp_sparse");
     mttkrp_sparse_kernel<<<(unsigned)grid, kSpWarps * 32, smem, call.stream()>>>(P);
     call.after_launch();
-    const int64_t nnz = call.read_scalar(P.total_nnz);
+    int64_t ctlv[3];
+    call.read_scalars(reinterpret_cast<int64_t*>(ctl), 3, ctlv);
+    const int64_t nnz = ctlv[2];
     call.finish_csr_result(A, nnz);
     call.finish();
     stam_stats* st = call.stats();
+    st->mults = ctlv[1];
+    st->adds = ctlv[1];
     st->ws_resets = B->nfibers + I;
     st->appends = nnz;
   });

@@ -118,3 +118,15 @@ def test_mttkrp_dimension_mismatch(ctx):
     with pytest.raises(StamError) as e:
         ctx.mttkrp(_d(cfg["B"]), _d(cfg["D"]), _d(cfg["C"]))
     assert e.value.code == "DimensionMismatch"
+
+
+def test_mttkrp_sparse_counters_match_reference_formula(ctx):
+    # SPEC.md:414-418 style counter: mults = sum over nonzeros of |D_k| (w0
+    # inserts) + consumed w0 entries (presence-checked w1 updates)
+    from paper_1802_10574_b200 import _native as N
+
+    cfg = G.make_config(5, scale=0.0005)
+    st = N.Stats()
+    ctx.mttkrp(_d(cfg["B"]), _d(cfg["C"]), _d(cfg["D"]), stats=st)
+    oracle.mttkrp_sparse(cfg["B"], cfg["C"], cfg["D"])
+    assert st.mults == oracle.last_counters()["mults"]
