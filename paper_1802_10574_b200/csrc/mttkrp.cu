@@ -19,11 +19,16 @@
 //           chunk are stored directly; slices cut by chunk boundaries leave
 //           per-chunk partials that a second kernel sums in chunk order
 //           (deterministic; no atomics on the heavy slices).
-//  sparse — one pass: ordered tiles of slices with decoupled look-back; a warp
-//           per slice, lanes over fibers; per fiber, w0 is evaluated only at
-//           C_j's stored coordinates (presence-checked lookups into the sorted
-//           D rows); w1 is a dense R-wide shared-memory workspace with a
-//           presence bitmap, drained sorted by ballot/popcount compaction.
+//  sparse — a warp per slice (claimed dynamically), lanes over fibers; per
+//           fiber, w0 is evaluated only at C_j's stored coordinates
+//           (presence-checked; the C_j and D_k column ids are held in
+//           registers and intersected all-pairs); w1 is a dense R-wide
+//           shared-memory workspace with a presence bitmap, drained sorted by
+//           ballot/popcount into a fixed-stride staging row (a row holds <= R
+//           entries); scan + coalesced compaction build the CSR.  (An ordered
+//           look-back made every slice wait for the slowest earlier one: 41% of
+//           warp samples asleep, profiles/r01_ncu_summary.md.)
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -389,6 +394,8 @@ struct SparseParams {
   unsigned long long* tile_counter;
   int64_t* total_nnz;
   unsigned long long* mults;  // SPEC counter: |D_k| per nonzero + consumed w0 entries
+  int64_t* stage_idx;         // [I*R] drained rows at a fixed stride
+  double* stage_vals;
 };
 
 __device__ __forceinline__ int64_t locate(const int64_t* a, int64_t n, int64_t x) {
@@ -477,8 +484,11 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
   }
 }
 
-// Warp-level ordered tiles: each warp claims a tile of kSpSlicesPerWarp
-// slices, evaluates them, looks back for its output offset and drains.
+// Each warp claims slices dynamically, evaluates one into its shared-memory
+// workspace and drains it sorted into a fixed-stride staging row (a row of A
+// holds at most R entries), recording the count in the row-pointer array.  No
+// ordering between slices is needed here; a scan and a coalesced compaction
+// copy build the CSR afterwards (no look-back waits on slower slices).
 __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const SparseParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = (int)lane_id();
@@ -486,64 +496,55 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const Spar
   const int64_t R = P.R;
   const int nwords = (int)((R + 31) / 32);
   const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
-  unsigned char* wbase = smem_raw + (size_t)warp * kSpSlicesPerWarp * ws_bytes;
+  double* wv = reinterpret_cast<double*>(smem_raw + (size_t)warp * ws_bytes);
+  uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
   unsigned long long mults = 0;
   while (true) {
-    int64_t tile = 0;
-    if (lane == 0) tile = (int64_t)atomicAdd(P.tile_counter, 1ull);
-    tile = __shfl_sync(kFull, tile, 0);
-    if (tile >= P.ntiles) break;
-    const int64_t i0 = tile * kSpSlicesPerWarp;
-    int64_t cnt[kSpSlicesPerWarp];
-#pragma unroll
-    for (int k = 0; k < kSpSlicesPerWarp; k++) {
-      double* wv = reinterpret_cast<double*>(wbase + k * ws_bytes);
-      uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
-      for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
-      for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
-      __syncwarp();
-      cnt[k] = 0;
-      if (i0 + k < P.I) {
-        sparse_slice(P, i0 + k, wv, wb, mults);
-        __syncwarp();
-        int64_t c = 0;
-        for (int w = lane; w < nwords; w += 32) c += __popc(wb[w]);
-        cnt[k] = warp_sum(c);
+    int64_t i = 0;
+    if (lane == 0) i = (int64_t)atomicAdd(P.tile_counter, 1ull);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= P.I) break;
+    for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
+    for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
+    __syncwarp();
+    sparse_slice(P, i, wv, wb, mults);
+    __syncwarp();
+    // sorted drain by ballot/popcount over the presence bitmap
+    int64_t* oi = P.stage_idx + i * R;
+    double* ov = P.stage_vals + i * R;
+    int out = 0;
+    for (int w = 0; w < nwords; w++) {
+      const uint32_t bits = wb[w];
+      if (bits == 0) continue;
+      if ((bits >> lane) & 1u) {
+        const int rank = __popc(bits & ((1u << lane) - 1u));
+        const int64_t r = (int64_t)w * 32 + lane;
+        oi[out + rank] = r;
+        ov[out + rank] = wv[r];
       }
+      out += __popc(bits);
     }
-    int64_t agg = 0;
-#pragma unroll
-    for (int k = 0; k < kSpSlicesPerWarp; k++) agg += cnt[k];
-    const int64_t base = lookback_exclusive(P.tile_status, tile, agg);
-    int64_t out = base;
-#pragma unroll
-    for (int k = 0; k < kSpSlicesPerWarp; k++) {
-      const int64_t i = i0 + k;
-      if (i >= P.I) break;
-      if (lane == 0) {
-        if (i == 0) P.out_pos[0] = 0;
-        P.out_pos[i + 1] = out + cnt[k];
-      }
-      const double* wv = reinterpret_cast<double*>(wbase + k * ws_bytes);
-      const uint32_t* wb = reinterpret_cast<const uint32_t*>(wv + R);
-      // sorted drain by ballot/popcount over the presence bitmap
-      for (int w = 0; w < nwords; w++) {
-        const uint32_t bits = wb[w];
-        if (bits == 0) continue;
-        if ((bits >> lane) & 1u) {
-          const int rank = __popc(bits & ((1u << lane) - 1u));
-          const int64_t r = (int64_t)w * 32 + lane;
-          P.out_idx[out + rank] = r;
-          P.out_vals[out + rank] = wv[r];
-        }
-        out += __popc(bits);
-      }
-    }
-    if (lane == 0 && tile == P.ntiles - 1) *P.total_nnz = base + agg;
+    if (lane == 0) P.out_pos[i + 1] = out;
     __syncwarp();
   }
   mults = warp_sum(mults);
   if (lane == 0 && mults) atomicAdd(P.mults, mults);
+}
+
+// Copies staged rows (stride R) into the compact CSR: a warp per row.
+__global__ void mttkrp_sparse_compact_kernel(const SparseParams P) {
+  const int lane = (int)lane_id();
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < P.I; i += nwarps) {
+    const int64_t dst = P.out_pos[i], n = P.out_pos[i + 1] - dst;
+    const int64_t* si = P.stage_idx + i * P.R;
+    const double* sv = P.stage_vals + i * P.R;
+    for (int64_t t = lane; t < n; t += 32) {
+      P.out_idx[dst + t] = si[t];
+      P.out_vals[dst + t] = sv[t];
+    }
+  }
 }
 
 }  // namespace
@@ -636,7 +637,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     if (Cv->ncols != Dv->ncols) fail(STAM_ERR_DIMENSION_MISMATCH, "mttkrp: C and D ranks differ");
     const int64_t I = B->dims[0], R = Cv->ncols;
     const size_t ws_bytes = (((size_t)R * 8 + (size_t)((R + 31) / 32) * 4) + 15) & ~(size_t)15;
-    const size_t smem = ws_bytes * kSpSlicesPerWarp * kSpWarps;
+    const size_t smem = ws_bytes * kSpWarps;
     if (smem > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "sparse mttkrp: rank too large for the shared-memory "
                                        "row workspace in ABI v1 (R <= ~1700)");
@@ -656,31 +657,46 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.dpos = call.device_input(Dv->pos, (size_t)Dv->nrows + 1, Dv->mem);
     P.didx = call.device_input(Dv->idx, (size_t)Dv->nnz, Dv->mem);
     P.dvals = call.device_input(Dv->vals, (size_t)Dv->nnz, Dv->mem);
-    P.ntiles = ceil_div(I, kSpSlicesPerWarp);
-    // a row of A has at most R entries: I*R bounds the output (no counting pass)
-    const int64_t bound = I * R;
-    call.alloc_csr_result(A, I, R, std::min<int64_t>(bound, (int64_t)1 << 40));
-    P.out_pos = A->pos;
-    P.out_idx = A->idx;
-    P.out_vals = A->vals;
-    auto* ctl = static_cast<uint64_t*>(call.scratch_zero((4 + (size_t)P.ntiles) * 8));
+    const size_t smem_w = ws_bytes * kSpWarps;
+    P.stage_idx = call.scratch_n<int64_t>((size_t)(I * R));
+    P.stage_vals = call.scratch_n<double>((size_t)(I * R));
+    auto* ctl = static_cast<uint64_t*>(call.scratch_zero(4 * 8));
     P.tile_counter = reinterpret_cast<unsigned long long*>(ctl);
     P.mults = reinterpret_cast<unsigned long long*>(ctl + 1);
-    P.total_nnz = reinterpret_cast<int64_t*>(ctl + 2);
-    P.tile_status = ctl + 4;
+    // row pointers: counts at [i+1], scanned in place
+    int64_t* cpos = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * ((size_t)I + 1)));
+    P.out_pos = cpos;
     STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
     int per_sm = 1;
     STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mttkrp_sparse_kernel,
-                                                                  kSpWarps * 32, smem));
-    const int64_t grid = std::min<int64_t>(ceil_div(P.ntiles, kSpWarps),
+                                                                  kSpWarps * 32, smem_w));
+    const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps),
                                            (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
     call.before_launch("mttkrp_sparse");
-    mttkrp_sparse_kernel<<<(unsigned)grid, kSpWarps * 32, smem, call.stream()>>>(P);
+    mttkrp_sparse_kernel<<<(unsigned)grid, kSpWarps * 32, smem_w, call.stream()>>>(P);
     call.after_launch();
-    int64_t ctlv[3];
-    call.read_scalars(reinterpret_cast<int64_t*>(ctl), 3, ctlv);
-    const int64_t nnz = ctlv[2];
+    size_t temp_bytes = 0;
+    STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, cpos + 1, cpos + 1, I,
+                                                  call.stream()));
+    void* temp = call.scratch(temp_bytes);
+    call.before_launch("mttkrp_sparse_scan");
+    STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(temp, temp_bytes, cpos + 1, cpos + 1, I,
+                                                  call.stream()));
+    call.after_launch();
+    int64_t ctlv[2];
+    call.read_scalars(reinterpret_cast<int64_t*>(ctl), 2, ctlv);
+    const int64_t nnz = call.read_scalar(cpos + I);
+    call.alloc_csr_result(A, I, R, nnz);
+    STAM_CUDA_CHECK(cudaMemcpyAsync(A->pos, cpos, sizeof(int64_t) * ((size_t)I + 1),
+                                    cudaMemcpyDeviceToDevice, call.stream()));
+    P.out_idx = A->idx;
+    P.out_vals = A->vals;
+    call.before_launch("mttkrp_sparse_compact");
+    mttkrp_sparse_compact_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 8),
+                                                               (int64_t)call.ctx()->num_sms * 16),
+                                   256, 0, call.stream()>>>(P);
+    call.after_launch();
     call.finish_csr_result(A, nnz);
     call.finish();
     stam_stats* st = call.stats();
