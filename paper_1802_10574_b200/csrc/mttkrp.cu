@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParam
               cbz = P.vals[zb + lane];
             }
           }
-          for (int t0 = 0; t0 < n; t0 += 16) {
+          int t0 = 0;
+          for (; t0 + 8 < n; t0 += 16) {  // 16 nonzeros: 8 independent row loads per lane
             double2 d[8];
             double b[8];
 #pragma unroll
@@ -217,6 +218,25 @@ __global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParam
             }
 #pragma unroll
             for (int u = 0; u < 8; u++) {
+              w0 = fma(b[u], d[u].x, w0);
+              w1 = fma(b[u], d[u].y, w1);
+            }
+          }
+          if (t0 < n) {  // tail of at most 8 nonzeros (most fibers are short)
+            double2 d[4];
+            double b[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const int src = t0 + 2 * u + half;
+              const int k = __shfl_sync(kFull, ckz, src & 31);
+              const double bv = __shfl_sync(kFull, cbz, src & 31);
+              const bool ok = src < n;
+              b[u] = ok ? bv : 0.0;
+              d[u] = ok ? __ldg(reinterpret_cast<const double2*>(P.D + (int64_t)k * 32 + col))
+                        : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
               w0 = fma(b[u], d[u].x, w0);
               w1 = fma(b[u], d[u].y, w1);
             }
@@ -324,7 +344,7 @@ __global__ void __launch_bounds__(256) mttkrp_dense_generic_kernel(const DensePa
 // one CTA per chain (the chunk holding the slice's tail partial plus the
 // following chunks holding its head partials); 8 warps take strided chunks,
 // then the 8 warp sums are added in warp order (deterministic).
-constexpr int kFixThreads = 256;
+constexpr int kFixThreads = 1024;
 __global__ void __launch_bounds__(kFixThreads) mttkrp_dense_fixup_kernel(const DenseParams P) {
   __shared__ int64_t end_sh;
   __shared__ double red[kFixThreads / 32][32];
@@ -349,8 +369,21 @@ __global__ void __launch_bounds__(kFixThreads) mttkrp_dense_fixup_kernel(const D
     const int64_t e = end_sh;
     for (int64_t cbi = 0; cbi < ncb; cbi++) {
       const double* base = P.part + cbi * P.nchunks * 64;
+      // 4 independent partial loads in flight per lane (order fixed per warp)
       double sum = 0.0;
-      for (int64_t c2 = c + 1 + warp; c2 < e; c2 += kFixThreads / 32)
+      constexpr int kW = kFixThreads / 32;
+      int64_t c2 = c + 1 + warp;
+      for (; c2 + 3 * kW < e; c2 += 4 * kW) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t cc = c2 + u * kW;
+          v[u] = P.part_slice[2 * cc] == s ? base[(cc * 2) * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) sum += v[u];
+      }
+      for (; c2 < e; c2 += kW)
         if (P.part_slice[2 * c2] == s) sum += base[(c2 * 2) * 32 + lane];
       red[warp][lane] = sum;
       __syncthreads();
@@ -489,7 +522,7 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
 // holds at most R entries), recording the count in the row-pointer array.  No
 // ordering between slices is needed here; a scan and a coalesced compaction
 // copy build the CSR afterwards (no look-back waits on slower slices).
-__global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_kernel(const SparseParams P) {
+__global__ void __launch_bounds__(kSpWarps * 32, 5) mttkrp_sparse_kernel(const SparseParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
