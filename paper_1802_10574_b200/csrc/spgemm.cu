@@ -439,6 +439,15 @@ struct HashSmem {
   int64_t claimed;
 };
 
+// The symbolic pass only needs the keys (3x less shared memory per row).
+template <int TB>
+struct HashKeysSmem {
+  uint32_t keys[TB + TB / 2];
+  int64_t red[2];
+  int scan[33];
+  int64_t claimed;
+};
+
 __device__ __forceinline__ int row_table(int64_t prod) {
   int tb = 64;
   while (tb < 2 * prod) tb <<= 1;
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(THREADS) hash_symbolic_kernel(const SpgemmPara
                                                                  int64_t nrows,
                                                                  unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  HashSmem<TB>& S = *reinterpret_cast<HashSmem<TB>*>(smem_raw);
+  HashKeysSmem<TB>& S = *reinterpret_cast<HashKeysSmem<TB>*>(smem_raw);
   while (true) {
     const int64_t r = claim_row<THREADS>(claim, &S.claimed);
     if (r >= nrows) break;
@@ -743,7 +752,7 @@ template <int THREADS, int TB>
 void launch_hash(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
                  bool numeric, const char* name, unsigned long long* claim) {
   if (n == 0) return;
-  const size_t smem = sizeof(HashSmem<TB>);
+  const size_t smem = numeric ? sizeof(HashSmem<TB>) : sizeof(HashKeysSmem<TB>);
   auto kern = numeric ? hash_numeric_kernel<THREADS, TB> : hash_symbolic_kernel<THREADS, TB>;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
