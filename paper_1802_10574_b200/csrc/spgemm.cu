@@ -506,43 +506,30 @@ __device__ __forceinline__ int run_boundary(const uint32_t* keys, int s0, int ns
   return nslots;
 }
 
-// Sorts every occupied run of the table and writes the occupied slots, in
-// slot order, to out_idx/out_vals.  Warps own contiguous slot ranges whose
-// ends sit on run boundaries; one block prefix over the warp counts.
+// Writes the occupied slots of the table in column order.  Runs (maximal
+// groups of consecutive occupied slots) are mutually ordered; inside a run an
+// entry's output position is the run's first position plus its rank among the
+// run's keys.  Warps own contiguous slot ranges whose ends sit on run
+// boundaries; one block prefix over the warp counts gives each warp its base.
+// A warp walks its range in windows of 32 slots cut after the window's last
+// empty slot, so every run in a window is complete and ranks come from warp
+// shuffles; runs of 32 or more slots rank through shared memory.
 template <int THREADS>
-__device__ void drain_table(uint32_t* keys, double* vals, int nslots, int64_t c0, int64_t* out_idx,
-                            double* out_vals, int* scan) {
+__device__ void drain_table(const uint32_t* keys, const double* vals, int nslots, int64_t c0,
+                            int64_t* out_idx, double* out_vals, int* scan) {
   constexpr int kWarpsN = THREADS / 32;
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
   const int per = (nslots + kWarpsN - 1) / kWarpsN;
   const int r0 = run_boundary(keys, warp * per, nslots);
   const int r1 = run_boundary(keys, (warp + 1) * per, nslots);
-  // sort the runs starting in [r0, r1) (lane per run start)
-  int cnt = 0;
-  for (int c = r0; c < r1; c += 32) {
-    const int s = c + lane;
-    const bool occ = s < r1 && keys[s] != kEmpty;
-    cnt += __popc(__ballot_sync(kFull, occ));
-    if (occ && (s == 0 || keys[s - 1] == kEmpty)) {
-      int e = s + 1;
-      while (e < nslots && keys[e] != kEmpty) e++;
-      for (int a = s + 1; a < e; a++) {
-        const uint32_t k = keys[a];
-        const double v = vals[a];
-        int b = a - 1;
-        while (b >= s && keys[b] > k) {
-          keys[b + 1] = keys[b];
-          vals[b + 1] = vals[b];
-          b--;
-        }
-        keys[b + 1] = k;
-        vals[b + 1] = v;
-      }
-    }
-  }
   int base = 0;
   if constexpr (kWarpsN > 1) {
+    int cnt = 0;
+    for (int c = r0; c < r1; c += 32) {
+      const int s = c + lane;
+      cnt += __popc(__ballot_sync(kFull, s < r1 && keys[s] != kEmpty));
+    }
     if (lane == 0) scan[warp] = cnt;
     __syncthreads();
     if (warp == 0) {
@@ -553,17 +540,68 @@ __device__ void drain_table(uint32_t* keys, double* vals, int nslots, int64_t c0
     __syncthreads();
     base = scan[warp];
   }
-  __syncwarp();
-  for (int c = r0; c < r1; c += 32) {
+  const unsigned lt = lanemask_lt();
+  int c = r0;
+  while (c < r1) {
     const int s = c + lane;
-    const bool occ = s < r1 && keys[s] != kEmpty;
-    const unsigned m = __ballot_sync(kFull, occ);
-    if (occ) {
-      const int pos = base + __popc(m & lanemask_lt());
-      out_idx[pos] = c0 + (int64_t)keys[s];
+    const uint32_t k = s < r1 ? keys[s] : kEmpty;
+    const bool occ = k != kEmpty;
+    const unsigned om = __ballot_sync(kFull, occ);
+    const unsigned em = ~om;
+    if (em == 0) {
+      // a run of >= 32 slots starting at c: find its end, rank in shared memory
+      int e = c + 32;
+      while (true) {
+        const int t = e + lane;
+        const unsigned m = __ballot_sync(kFull, t >= r1 || keys[t] == kEmpty);
+        if (m) {
+          e += __ffs(m) - 1;
+          break;
+        }
+        e += 32;
+      }
+      const int len = e - c;
+      for (int x = lane; x < len + (32 - len % 32) % 32; x += 32) {
+        const bool mine = x < len;
+        const uint32_t kx = mine ? keys[c + x] : kEmpty;
+        int rank = 0;
+        for (int j = 0; j < len; j++) rank += keys[c + j] < kx ? 1 : 0;
+        if (mine) {
+          out_idx[base + rank] = c0 + (int64_t)kx;
+          out_vals[base + rank] = vals[c + x];
+        }
+      }
+      base += len;
+      c = e;
+      continue;
+    }
+    const int last = 31 - __clz(em);  // the window's last empty slot
+    const bool mine = occ && lane < last;
+    const unsigned below = em & lt;
+    const int rs = below ? 32 - __clz(below) : 0;  // my run's first lane
+    const unsigned above = em & ~(lt | (1u << lane));
+    const int re = __ffs(above) - 1;  // my run's end (an empty lane <= last)
+    // ranks: only windows whose runs are out of order need the shuffle loop
+    const uint32_t kprev = __shfl_up_sync(kFull, k, 1);
+    const bool dis = mine && lane > rs && kprev > k;
+    int rank = lane - rs;
+    if (__any_sync(kFull, dis)) {
+      const int len = mine ? re - rs : 0;
+      const int maxl = __reduce_max_sync(kFull, (unsigned)len);
+      rank = 0;
+      for (int d = 0; d < maxl; d++) {
+        const int src = rs + d;
+        const uint32_t kk = __shfl_sync(kFull, k, src & 31);
+        rank += (src < re && kk < k) ? 1 : 0;
+      }
+    }
+    if (mine) {
+      const int pos = base + __popc(om & ((1u << rs) - 1)) + rank;
+      out_idx[pos] = c0 + (int64_t)k;
       out_vals[pos] = vals[s];
     }
-    base += __popc(m);
+    base += __popc(om & ((1u << last) - 1));
+    c += last + 1;
   }
 }
 
