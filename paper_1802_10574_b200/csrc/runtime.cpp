@@ -30,6 +30,15 @@ Call::Call(Ctx* ctx, const stam_options* opts, stam_stats* stats) : ctx_(ctx) {
 
 Call::~Call() {
   // Temporaries go back to the pool in stream order; nothing here may throw.
+  if (copies_open_ && ctx_->event_next < ctx_->event_pool.size()) {
+    // staging copies still in flight must land before their buffers are freed
+    cudaEvent_t ev = ctx_->event_pool[ctx_->event_next++];
+    cudaEventRecord(ev, ctx_->copy_stream);
+    cudaStreamWaitEvent(ctx_->stream, ev, 0);
+  } else if (copies_open_) {
+    cudaStreamSynchronize(ctx_->copy_stream);
+  }
+  if (d2h_open_) cudaStreamSynchronize(ctx_->d2h_stream);
   for (void* p : temps_) cudaFreeAsync(p, ctx_->stream);
   if (!finished_) cudaStreamSynchronize(ctx_->stream);
 }
@@ -63,6 +72,39 @@ const void* Call::stage(const void* p, size_t bytes, int32_t mem) {
   if (opts_.timing) STAM_CUDA_CHECK(cudaEventRecord(h2d_stop_, ctx_->stream));
   return d;
 }
+
+cudaEvent_t Call::event() {
+  if (ctx_->event_next + 1 > ctx_->event_pool.size()) {
+    for (int e = 0; e < 64; e++) {
+      cudaEvent_t ev;
+      STAM_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ctx_->event_pool.push_back(ev);
+    }
+  }
+  return ctx_->event_pool[ctx_->event_next++];
+}
+
+void Call::copy_range(void* dst, const void* src, size_t bytes) {
+  if (!ctx_->copy_stream)
+    STAM_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx_->copy_stream, cudaStreamNonBlocking));
+  if (!copies_open_) {
+    // the staging buffers were allocated in kernel-stream order
+    cudaEvent_t ready = event();
+    STAM_CUDA_CHECK(cudaEventRecord(ready, ctx_->stream));
+    STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->copy_stream, ready, 0));
+    copies_open_ = true;
+  }
+  if (bytes)
+    STAM_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx_->copy_stream));
+}
+
+cudaEvent_t Call::copy_fence() {
+  cudaEvent_t ev = event();
+  STAM_CUDA_CHECK(cudaEventRecord(ev, ctx_->copy_stream ? ctx_->copy_stream : ctx_->stream));
+  return ev;
+}
+
+void Call::wait(cudaEvent_t ev) { STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->stream, ev, 0)); }
 
 void Call::before_launch(const char* name) {
   stats_->kernel_launches++;
@@ -144,6 +186,61 @@ void Call::alloc_csr_result(stam_csr_result* r, int64_t nrows, int64_t ncols,
   r->idx = (int64_t*)((char*)d + pos_b);
   r->vals = (double*)((char*)d + pos_b + idx_b);
   r->mem = STAM_MEM_DEVICE;
+}
+
+void Call::alloc_csr_result_streamed(stam_csr_result* r, int64_t nrows, int64_t ncols,
+                                     int64_t nnz_capacity, int64_t** hpos, int64_t** hidx,
+                                     double** hvals) {
+  alloc_csr_result(r, nrows, ncols, nnz_capacity);
+  auto* own = static_cast<Owned*>(r->handle);
+  const size_t pos_b = align_up((size_t)(nrows + 1) * sizeof(int64_t), 256);
+  const size_t idx_b = align_up((size_t)std::max<int64_t>(nnz_capacity, 1) * sizeof(int64_t), 256);
+  const size_t val_b = align_up((size_t)std::max<int64_t>(nnz_capacity, 1) * sizeof(double), 256);
+  char* h = static_cast<char*>(pinned_alloc(pos_b + idx_b + val_b));
+  own->host_pending = h;
+  own->host_bytes = pos_b + idx_b + val_b;
+  *hpos = (int64_t*)h;
+  *hidx = (int64_t*)(h + pos_b);
+  *hvals = (double*)(h + pos_b + idx_b);
+}
+
+void Call::d2h_range(void* dst, const void* src, size_t bytes, cudaEvent_t ready) {
+  if (!ctx_->d2h_stream)
+    STAM_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx_->d2h_stream, cudaStreamNonBlocking));
+  if (ready) STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->d2h_stream, ready, 0));
+  d2h_open_ = true;
+  if (bytes)
+    STAM_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx_->d2h_stream));
+}
+
+void Call::finish_csr_result_streamed(stam_csr_result* r, int64_t nnz) {
+  auto* own = static_cast<Owned*>(r->handle);
+  r->nnz = nnz;
+  if (d2h_open_) {
+    cudaEvent_t done = event();
+    STAM_CUDA_CHECK(cudaEventRecord(done, ctx_->d2h_stream));
+    STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->stream, done, 0));
+  }
+  char* h = static_cast<char*>(own->host_pending);
+  const size_t pos_b = align_up((size_t)(r->nrows + 1) * sizeof(int64_t), 256);
+  const size_t idx_b = (size_t)((char*)r->vals - (char*)r->idx);
+  STAM_CUDA_CHECK(cudaFreeAsync(own->dev, ctx_->stream));
+  own->dev = nullptr;
+  own->host = h;
+  own->host_pending = nullptr;
+  r->pos = (int64_t*)h;
+  r->idx = (int64_t*)(h + pos_b);
+  r->vals = (double*)(h + pos_b + idx_b);
+  r->mem = STAM_MEM_HOST;
+}
+
+int64_t* Call::marks() {
+  if (!ctx_->h_marks) {
+    void* p = nullptr;
+    STAM_CUDA_CHECK(cudaHostAlloc(&p, Ctx::kMarks * sizeof(int64_t), cudaHostAllocMapped));
+    ctx_->h_marks = static_cast<int64_t*>(p);
+  }
+  return ctx_->h_marks;
 }
 
 void Call::finish_csr_result(stam_csr_result* r, int64_t nnz) {
@@ -241,6 +338,42 @@ void Call::finish() {
 }
 
 // ---------------------------------------------------------------------------
+std::vector<int64_t> stream_blocks(int64_t nunits, int64_t total_bytes, int64_t steady_bytes,
+                                   int64_t max_blocks) {
+  std::vector<int64_t> b{0};
+  if (nunits <= 0) {
+    b.push_back(0);
+    return b;
+  }
+  const double per_unit = std::max(1.0, (double)total_bytes / (double)nunits);
+  // ramp 1/16, 1/8, 1/4, 1/2 of the steady size at both ends
+  std::vector<int64_t> sizes;
+  int64_t left = total_bytes;
+  std::vector<int64_t> tail;
+  for (int64_t s = steady_bytes / 16; s < steady_bytes && left > 4 * s; s *= 2) {
+    sizes.push_back(s);
+    tail.push_back(s);
+    left -= 2 * s;
+  }
+  while (left > 0) {
+    sizes.push_back(std::min(left, steady_bytes));
+    left -= steady_bytes;
+  }
+  for (auto it = tail.rbegin(); it != tail.rend(); ++it) sizes.push_back(*it);
+  if ((int64_t)sizes.size() > max_blocks) {
+    sizes.assign((size_t)max_blocks, (total_bytes + max_blocks - 1) / max_blocks);
+  }
+  double acc = 0.0;
+  for (int64_t s : sizes) {
+    acc += (double)s;
+    const int64_t u = std::min<int64_t>(nunits, std::max<int64_t>(b.back() + 1, (int64_t)(acc / per_unit)));
+    if (u > b.back()) b.push_back(u);
+    if (b.back() == nunits) break;
+  }
+  if (b.back() != nunits) b.push_back(nunits);
+  return b;
+}
+
 void check_csr_view(const stam_csr_view* v, const char* what) {
   if (!v) fail(STAM_ERR_PRECONDITION_VIOLATED, std::string(what) + ": null view");
   if (v->nrows <= 0 || v->ncols <= 0)
@@ -340,6 +473,9 @@ int stam_cuda_ctx_destroy(stam_cuda_ctx* ctx) {
     for (auto ev : ctx->event_pool) cudaEventDestroy(ev);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+    if (ctx->h_marks) cudaFreeHost(ctx->h_marks);
     delete ctx;
   });
 }
@@ -368,6 +504,7 @@ int stam_cuda_release(stam_cuda_ctx* ctx, void* handle) {
     auto* own = static_cast<Owned*>(handle);
     STAM_CUDA_CHECK(cudaSetDevice(ctx->device));
     if (own->dev) STAM_CUDA_CHECK(cudaFreeAsync(own->dev, ctx->stream));
+    if (own->host_pending && !own->host) own->host = own->host_pending;
     if (own->host) {
       // keep a bounded cache of pinned buffers (pinning is slow)
       ctx->pinned_free.emplace_back(own->host, own->host_bytes);

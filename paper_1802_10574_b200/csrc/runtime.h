@@ -46,6 +46,12 @@ struct Ctx {
   size_t smem_optin = 227 * 1024;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host->device staging overlapped with kernels
+  cudaStream_t d2h_stream = nullptr;   // device->host result blocks overlapped with kernels
+  // pinned, device-mapped marks written by kernels (e.g. a row block's end
+  // offset) and read by the host after the block's event
+  int64_t* h_marks = nullptr;
+  static constexpr int kMarks = 128;
   cudaMemPool_t pool = nullptr;
   // pinned host memory returned by released host results, reused by size
   std::vector<std::pair<void*, size_t>> pinned_free;
@@ -60,6 +66,7 @@ struct Owned {
   void* dev = nullptr;
   void* host = nullptr;
   size_t host_bytes = 0;
+  void* host_pending = nullptr;  // streamed host buffer, handed out by finish
 };
 
 // Per-call state: temporary device allocations (freed stream-ordered at the
@@ -88,6 +95,18 @@ class Call {
     return static_cast<const T*>(stage(p, n * sizeof(T), mem));
   }
 
+  // Streamed staging: a device buffer for a host array whose ranges are
+  // copied on the context's copy stream (copy_range), each batch of copies
+  // closed by copy_fence() -> an event the kernel stream waits on.
+  template <typename T>
+  T* host_staging(size_t n) {
+    return static_cast<T*>(scratch(n * sizeof(T)));
+  }
+  void copy_range(void* dst, const void* src, size_t bytes);
+  cudaEvent_t copy_fence();
+  void wait(cudaEvent_t ev);
+  cudaEvent_t event();
+
   // Launch bookkeeping: call before/after each kernel launch.
   void before_launch(const char* name);
   void after_launch();
@@ -99,6 +118,16 @@ class Call {
   // Result buffers: one device block holding pos/idx/vals (or vals only).
   void alloc_csr_result(stam_csr_result* r, int64_t nrows, int64_t ncols, int64_t nnz_capacity);
   void finish_csr_result(stam_csr_result* r, int64_t nnz);
+  // Host result filled block by block while later blocks compute: device
+  // result + a pinned host buffer of the same capacity; d2h_range copies a
+  // finished range on the d2h stream (after `ready`), finish_csr_result_streamed
+  // joins the copies and hands out the host buffer.
+  void alloc_csr_result_streamed(stam_csr_result* r, int64_t nrows, int64_t ncols,
+                                 int64_t nnz_capacity, int64_t** hpos, int64_t** hidx,
+                                 double** hvals);
+  void d2h_range(void* dst, const void* src, size_t bytes, cudaEvent_t ready);
+  void finish_csr_result_streamed(stam_csr_result* r, int64_t nnz);
+  int64_t* marks();
   void alloc_dense_result(stam_dense_result* r, int64_t nrows, int64_t ncols);
   void finish_dense_result(stam_dense_result* r);
 
@@ -120,6 +149,8 @@ class Call {
   cudaEvent_t h2d_start_ = nullptr, h2d_stop_ = nullptr;
   cudaEvent_t d2h_start_ = nullptr, d2h_stop_ = nullptr;
   bool finished_ = false;
+  bool copies_open_ = false;
+  bool d2h_open_ = false;
   int pending_ = -1;
 };
 
@@ -142,6 +173,13 @@ int guarded(F&& fn) {
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Block boundaries (in units, first 0, last nunits) for a streamed call
+// moving `total_bytes` spread evenly over `nunits`: small blocks first and
+// last (short pipeline fill and drain), `steady_bytes` blocks in between,
+// at most max_blocks blocks.
+std::vector<int64_t> stream_blocks(int64_t nunits, int64_t total_bytes, int64_t steady_bytes,
+                                   int64_t max_blocks);
 
 // Validates a CSR view's scalar fields (array contents are trusted; the C++
 // wrapper validates storage before calling, as TensorStorage::validate does).

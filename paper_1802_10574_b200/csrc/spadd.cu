@@ -22,7 +22,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "runtime.h"
@@ -45,6 +47,9 @@ struct SpaddParams {
   int nops;
   int64_t nrows;
   int64_t ntiles;
+  int64_t tile_base;  // first tile of this launch (row blocks of a streamed call)
+  int64_t last_tile;  // last tile of this launch: publishes its end offset
+  int64_t* block_end; // (host-mapped) end offset of this launch's rows
   int64_t* out_pos;
   int64_t* out_idx;
   double* out_vals;
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(kWarps * 32) spadd_tiles_kernel(const SpaddPar
   const int warp = threadIdx.x >> 5;
   const int nops = P.nops;
 
-  if (threadIdx.x == 0) S.tile_id = (int64_t)atomicAdd(P.tile_counter, 1ull);
+  if (threadIdx.x == 0) S.tile_id = P.tile_base + (int64_t)atomicAdd(P.tile_counter, 1ull);
   __syncthreads();
   const int64_t tile = S.tile_id;
   const int64_t row0 = tile * kTileRows;
@@ -339,6 +344,7 @@ __global__ void __launch_bounds__(kWarps * 32) spadd_tiles_kernel(const SpaddPar
     if (lane == 0) {
       if (tile == 0) P.out_pos[0] = 0;
       if (tile == P.ntiles - 1) *P.total_nnz = base + agg;
+      if (tile == P.last_tile && P.block_end) *P.block_end = base + agg;
     }
   }
   __syncthreads();
@@ -465,12 +471,13 @@ __global__ void __launch_bounds__(kLongThreads) spadd_long_rows_kernel(const Spa
 }
 
 template <typename ColT>
-void launch_tiles(stamrt::Call& call, const SpaddParams& P) {
+void launch_tiles(stamrt::Call& call, const SpaddParams& P, int64_t ntiles) {
+  if (ntiles <= 0) return;
   const size_t smem = sizeof(TileSmem<ColT>);
   auto kern = spadd_tiles_kernel<ColT>;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   call.before_launch(sizeof(ColT) == 4 ? "spadd_tiles<u32>" : "spadd_tiles<i64>");
-  kern<<<(unsigned)P.ntiles, kWarps * 32, smem, call.stream()>>>(P);
+  kern<<<(unsigned)ntiles, kWarps * 32, smem, call.stream()>>>(P);
   call.after_launch();
 }
 
@@ -499,40 +506,129 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     SpaddParams P{};
     P.nops = nops;
     P.nrows = nrows;
-    int64_t cap = 0, accum = 0;
+    P.ntiles = ceil_div(nrows, kTileRows);
+    int64_t cap = 0, accum = 0, in_bytes = 0;
+    bool host_in = false;
     for (int p = 0; p < nops; p++) {
-      P.pos[p] = call.device_input(ops[p].pos, (size_t)nrows + 1, ops[p].mem);
-      P.idx[p] = call.device_input(ops[p].idx, (size_t)ops[p].nnz, ops[p].mem);
-      P.vals[p] = call.device_input(ops[p].vals, (size_t)ops[p].nnz, ops[p].mem);
       cap += ops[p].nnz;
       if (p > 0) accum += ops[p].nnz;
+      host_in |= ops[p].mem == STAM_MEM_HOST;
+      in_bytes += ops[p].nnz * 16;
     }
-    P.ntiles = ceil_div(nrows, kTileRows);
-    call.alloc_csr_result(D, nrows, ncols, cap);
+    const bool host_out = call.opts().result_mem == STAM_MEM_HOST;
+    // Host operands or a host result: stream row blocks.  Block k's operand
+    // ranges go up on the copy stream while earlier blocks merge, and each
+    // finished block's output range comes down on the d2h stream while later
+    // blocks merge (PCIe carries both directions at once).
+    std::vector<int64_t> blk{0, P.ntiles};  // block boundaries in tiles
+    if (host_in || host_out) {
+      int64_t block_mb = 64;
+      if (const char* e = std::getenv("STAM_STREAM_BLOCK_MB")) block_mb = std::max(1, std::atoi(e));
+      blk = stream_blocks(P.ntiles, in_bytes, block_mb << 20, Ctx::kMarks);
+    }
+    const int64_t nblocks = (int64_t)blk.size() - 1;
+    const int64_t* hpos[kMaxOps] = {};
+    for (int p = 0; p < nops; p++) {
+      P.pos[p] = call.device_input(ops[p].pos, (size_t)nrows + 1, ops[p].mem);
+      if (ops[p].mem == STAM_MEM_HOST) {
+        hpos[p] = ops[p].pos;
+        P.idx[p] = call.host_staging<int64_t>((size_t)ops[p].nnz);
+        P.vals[p] = call.host_staging<double>((size_t)ops[p].nnz);
+      } else {
+        P.idx[p] = ops[p].idx;
+        P.vals[p] = ops[p].vals;
+      }
+    }
+    int64_t* h_pos = nullptr;
+    int64_t* h_idx = nullptr;
+    double* h_vals = nullptr;
+    if (host_out)
+      call.alloc_csr_result_streamed(D, nrows, ncols, cap, &h_pos, &h_idx, &h_vals);
+    else
+      call.alloc_csr_result(D, nrows, ncols, cap);
     P.out_pos = D->pos;
     P.out_idx = D->idx;
     P.out_vals = D->vals;
-    // control block: [tile counter, deferred count, total] + tile status words
-    const size_t ctl_words = 4 + (size_t)P.ntiles;
+    // control block: [deferred count, total, pad, pad] + one tile counter per
+    // block + tile status words
+    const size_t ctl_words = 4 + (size_t)nblocks + (size_t)P.ntiles;
     auto* ctl = static_cast<uint64_t*>(call.scratch_zero(ctl_words * sizeof(uint64_t)));
-    P.tile_counter = reinterpret_cast<unsigned long long*>(ctl);
-    P.deferred_count = reinterpret_cast<unsigned long long*>(ctl + 1);
-    P.total_nnz = reinterpret_cast<int64_t*>(ctl + 2);
-    P.tile_status = ctl + 4;
+    P.deferred_count = reinterpret_cast<unsigned long long*>(ctl);
+    P.total_nnz = reinterpret_cast<int64_t*>(ctl + 1);
+    P.tile_status = ctl + 4 + nblocks;
     const int64_t max_deferred = std::min<int64_t>(nrows, cap / kStage + 1);
     P.deferred_rows = call.scratch_n<int64_t>((size_t)max_deferred);
+    int64_t* marks = host_out ? call.marks() : nullptr;
 
-    if (ncols <= (int64_t)UINT32_MAX)
-      launch_tiles<uint32_t>(call, P);
-    else
-      launch_tiles<int64_t>(call, P);
+    std::vector<cudaEvent_t> done((size_t)nblocks);
+    auto issue_block = [&](int64_t k) {
+      const int64_t t0 = blk[(size_t)k];
+      const int64_t t1 = blk[(size_t)k + 1];
+      if (host_in) {
+        const int64_t r0 = t0 * kTileRows, r1 = std::min(nrows, t1 * kTileRows);
+        for (int p = 0; p < nops; p++) {
+          if (!hpos[p]) continue;
+          const int64_t e0 = hpos[p][r0], e1 = hpos[p][r1];
+          call.copy_range(const_cast<int64_t*>(P.idx[p]) + e0, ops[p].idx + e0,
+                          (size_t)(e1 - e0) * sizeof(int64_t));
+          call.copy_range(const_cast<double*>(P.vals[p]) + e0, ops[p].vals + e0,
+                          (size_t)(e1 - e0) * sizeof(double));
+        }
+        call.wait(call.copy_fence());
+      }
+      P.tile_base = t0;
+      P.last_tile = t1 - 1;
+      P.block_end = marks ? marks + k : nullptr;
+      P.tile_counter = reinterpret_cast<unsigned long long*>(ctl + 4 + k);
+      if (ncols <= (int64_t)UINT32_MAX)
+        launch_tiles<uint32_t>(call, P, t1 - t0);
+      else
+        launch_tiles<int64_t>(call, P, t1 - t0);
+      if (host_out) {
+        done[(size_t)k] = call.event();
+        STAM_CUDA_CHECK(cudaEventRecord(done[(size_t)k], call.stream()));
+      }
+    };
+    if (!host_out) {
+      for (int64_t k = 0; k < nblocks; k++) issue_block(k);
+    } else {
+      // keep a few blocks of uploads ahead; bring finished blocks down while
+      // later ones compute (uploads and downloads interleave in issue order)
+      constexpr int64_t kAhead = 3;
+      int64_t issued = 0, prev = 0;
+      for (; issued < std::min(nblocks, kAhead); issued++) issue_block(issued);
+      for (int64_t k = 0; k < nblocks; k++) {
+        STAM_CUDA_CHECK(cudaEventSynchronize(done[(size_t)k]));
+        const int64_t end = *(volatile int64_t*)(marks + k);
+        const int64_t r0 = blk[(size_t)k] * kTileRows;
+        const int64_t r1 = std::min(nrows, blk[(size_t)k + 1] * kTileRows);
+        call.d2h_range(h_pos + r0 + (k == 0 ? 0 : 1), D->pos + r0 + (k == 0 ? 0 : 1),
+                       (size_t)(r1 - r0 + (k == 0 ? 1 : 0)) * sizeof(int64_t), done[(size_t)k]);
+        call.d2h_range(h_idx + prev, D->idx + prev, (size_t)(end - prev) * sizeof(int64_t), nullptr);
+        call.d2h_range(h_vals + prev, D->vals + prev, (size_t)(end - prev) * sizeof(double), nullptr);
+        prev = end;
+        if (issued < nblocks) issue_block(issued++);
+      }
+    }
+    // rows too long for a warp's staging (deferred by their tiles)
     call.before_launch("spadd_long_rows");
     spadd_long_rows_kernel<<<(unsigned)std::max(1, call.ctx()->num_sms), kLongThreads, 0,
                              call.stream()>>>(P);
     call.after_launch();
-
-    const int64_t nnz = call.read_scalar(P.total_nnz);
-    call.finish_csr_result(D, nnz);
+    int64_t tail[2];
+    call.read_scalars(reinterpret_cast<const int64_t*>(ctl), 2, tail);  // deferred, total
+    const int64_t nnz = tail[1];
+    if (host_out) {
+      if (tail[0] > 0) {
+        // long rows were filled after their blocks came down (the stream
+        // was synchronised above): bring the entries down again
+        call.d2h_range(h_idx, D->idx, (size_t)nnz * sizeof(int64_t), nullptr);
+        call.d2h_range(h_vals, D->vals, (size_t)nnz * sizeof(double), nullptr);
+      }
+      call.finish_csr_result_streamed(D, nnz);
+    } else {
+      call.finish_csr_result(D, nnz);
+    }
     call.finish();
     stam_stats* st = call.stats();
     st->adds = accum;
