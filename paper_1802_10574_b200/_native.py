@@ -7,6 +7,7 @@ the product path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -120,7 +121,9 @@ class StamError(RuntimeError):
 
 
 def library_path() -> Path:
-    return _LIB_DIR / "libstam_cuda.so"
+    # STAM_CUDA_LIB: an alternative build of the same library (tuning variants)
+    alt = os.environ.get("STAM_CUDA_LIB")
+    return Path(alt) if alt else _LIB_DIR / "libstam_cuda.so"
 
 
 def load() -> C.CDLL:
