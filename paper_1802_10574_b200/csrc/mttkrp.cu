@@ -429,6 +429,9 @@ struct SparseParams {
   unsigned long long* mults;  // SPEC counter: |D_k| per nonzero + consumed w0 entries
   int64_t* stage_idx;         // [I*R] drained rows at a fixed stride
   double* stage_vals;
+  // column bitmaps of the factor rows (kBmWords 64-bit words per row; R <= 64*W)
+  const unsigned long long* cbm;
+  const unsigned long long* dbm;
 };
 
 __device__ __forceinline__ int64_t locate(const int64_t* a, int64_t n, int64_t x) {
@@ -517,11 +520,145 @@ __device__ void sparse_slice(const SparseParams& P, int64_t i, double* wv, uint3
   }
 }
 
+// Column bitmap of every factor row: W 64-bit words per row (bit r = column
+// r present).  One thread per row; rows hold sorted distinct columns.
+template <int W>
+__global__ void factor_bitmap_kernel(const int64_t* pos, const int64_t* idx, int64_t nrows,
+                                     unsigned long long* bm) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long w[W];
+#pragma unroll
+    for (int k = 0; k < W; k++) w[k] = 0ull;
+    for (int64_t t = pos[r]; t < pos[r + 1]; t++) {
+      const int64_t c = idx[t];
+#pragma unroll
+      for (int k = 0; k < W; k++) w[k] |= ((c >> 6) == k) ? (1ull << (c & 63)) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < W; k++) bm[r * W + k] = w[k];
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void load_bm(const unsigned long long* p, unsigned long long (&b)[W]) {
+  if constexpr (W % 2 == 0) {
+#pragma unroll
+    for (int k = 0; k < W; k += 2) {
+      const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p) + k / 2);
+      b[k] = v.x;
+      b[k + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; k++) b[k] = __ldg(p + k);
+  }
+}
+
+// Position of column r among the row's columns (popcount of the bits below).
+template <int W>
+__device__ __forceinline__ int bm_rank(const unsigned long long (&b)[W], int r) {
+  int n = 0;
+#pragma unroll
+  for (int k = 0; k < W; k++) {
+    const int lo = k * 64;
+    if (r >= lo + 64) n += __popcll(b[k]);
+    else if (r > lo) n += __popcll(b[k] & ((1ull << (r - lo)) - 1ull));
+  }
+  return n;
+}
+
+// sparse_slice with factor-row bitmaps: C_j ∩ D_k is a word-wise AND, a
+// matched column's value positions are popcounts, and value loads happen
+// only for matches (same arithmetic and order as sparse_slice).
+template <int W>
+__device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, uint32_t* wb,
+                                unsigned long long& mults) {
+  const int lane = (int)lane_id();
+  const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
+  for (int64_t f = f0 + lane; f < f1; f += 32) {
+    const int64_t j = P.idx1[f];
+    const int64_t z0 = P.pos2[f], z1 = P.pos2[f + 1];
+    unsigned long long bc[W];
+    load_bm<W>(P.cbm + j * W, bc);
+    if (z1 - z0 == 1) {
+      const int64_t k = P.idx2[z0];
+      const double b = P.vals[z0];
+      unsigned long long bd[W];
+      load_bm<W>(P.dbm + k * W, bd);
+      unsigned long long any = 0ull;
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        mults += (unsigned long long)__popcll(bd[w]);
+        any |= bc[w] & bd[w];
+      }
+      if (any) {
+        const int64_t c0 = P.cpos[j], d0 = P.dpos[k];
+        int rc = 0, rd = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          unsigned long long m = bc[w] & bd[w];
+          while (m) {
+            const int bit = __ffsll((long long)m) - 1;
+            const unsigned long long below = (1ull << bit) - 1ull;
+            const int ic = rc + __popcll(bc[w] & below);
+            const int id = rd + __popcll(bd[w] & below);
+            // w0(r) = 0 + b*D(k,r);  w1(r) += w0(r)*C(j,r)
+            const double w0 = add_rn(0.0, mul_rn(b, P.dvals[d0 + id]));
+            ws_add(wv, wb, w * 64 + bit, mul_rn(w0, P.cvals[c0 + ic]));
+            mults++;
+            m &= m - 1ull;
+          }
+          rc += __popcll(bc[w]);
+          rd += __popcll(bd[w]);
+        }
+      }
+    } else {
+      // general fiber: w0 at each of C_j's columns, accumulated over k in order
+      for (int64_t z = z0; z < z1; z++) {
+        const int64_t k = P.idx2[z];
+        unsigned long long bd[W];
+        load_bm<W>(P.dbm + k * W, bd);
+#pragma unroll
+        for (int w = 0; w < W; w++) mults += (unsigned long long)__popcll(bd[w]);
+      }
+      const int64_t c0 = P.cpos[j];
+      int ic = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        unsigned long long m = bc[w];
+        while (m) {
+          const int bit = __ffsll((long long)m) - 1;
+          const int r = w * 64 + bit;
+          double w0 = 0.0;
+          bool present = false;
+          for (int64_t z = z0; z < z1; z++) {
+            const int64_t k = P.idx2[z];
+            unsigned long long bd[W];
+            load_bm<W>(P.dbm + k * W, bd);
+            if ((bd[w] >> bit) & 1ull) {
+              w0 = add_rn(w0, mul_rn(P.vals[z], P.dvals[P.dpos[k] + bm_rank<W>(bd, r)]));
+              present = true;
+            }
+          }
+          if (present) {
+            ws_add(wv, wb, r, mul_rn(w0, P.cvals[c0 + ic]));
+            mults++;
+          }
+          ic++;
+          m &= m - 1ull;
+        }
+      }
+    }
+  }
+}
+
 // Each warp claims slices dynamically, evaluates one into its shared-memory
 // workspace and drains it sorted into a fixed-stride staging row (a row of A
 // holds at most R entries), recording the count in the row-pointer array.  No
 // ordering between slices is needed here; a scan and a coalesced compaction
 // copy build the CSR afterwards (no look-back waits on slower slices).
+template <int W>
 __global__ void __launch_bounds__(kSpWarps * 32, 5) mttkrp_sparse_kernel(const SparseParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = (int)lane_id();
@@ -540,7 +677,10 @@ __global__ void __launch_bounds__(kSpWarps * 32, 5) mttkrp_sparse_kernel(const S
     for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
     for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
     __syncwarp();
-    sparse_slice(P, i, wv, wb, mults);
+    if constexpr (W > 0)
+      sparse_slice_bm<W>(P, i, wv, wb, mults);
+    else
+      sparse_slice(P, i, wv, wb, mults);
     __syncwarp();
     // sorted drain by ballot/popcount over the presence bitmap
     int64_t* oi = P.stage_idx + i * R;
@@ -699,16 +839,46 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     // row pointers: counts at [i+1], scanned in place
     int64_t* cpos = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * ((size_t)I + 1)));
     P.out_pos = cpos;
-    STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
-    int per_sm = 1;
-    STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mttkrp_sparse_kernel,
-                                                                  kSpWarps * 32, smem_w));
-    const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps),
-                                           (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
-    call.before_launch("mttkrp_sparse");
-    mttkrp_sparse_kernel<<<(unsigned)grid, kSpWarps * 32, smem_w, call.stream()>>>(P);
-    call.after_launch();
+    // factor-row column bitmaps when R fits W <= 8 words
+    const int64_t words = (R + 63) / 64;
+    const int W = words <= 1 ? 1 : words <= 2 ? 2 : words <= 4 ? 4 : words <= 8 ? 8 : 0;
+    auto build_bm = [&](const int64_t* pos, const int64_t* idx, int64_t nrows) {
+      auto* bm = call.scratch_n<unsigned long long>((size_t)(nrows * W));
+      const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nrows, 256),
+                                                        (int64_t)call.ctx()->num_sms * 8);
+      call.before_launch("mttkrp_factor_bitmap");
+      switch (W) {
+        case 1: factor_bitmap_kernel<1><<<grid, 256, 0, call.stream()>>>(pos, idx, nrows, bm); break;
+        case 2: factor_bitmap_kernel<2><<<grid, 256, 0, call.stream()>>>(pos, idx, nrows, bm); break;
+        case 4: factor_bitmap_kernel<4><<<grid, 256, 0, call.stream()>>>(pos, idx, nrows, bm); break;
+        default: factor_bitmap_kernel<8><<<grid, 256, 0, call.stream()>>>(pos, idx, nrows, bm); break;
+      }
+      call.after_launch();
+      return bm;
+    };
+    if (W > 0) {
+      P.cbm = build_bm(P.cpos, P.cidx, Cv->nrows);
+      P.dbm = build_bm(P.dpos, P.didx, Dv->nrows);
+    }
+    auto launch = [&](auto kern) {
+      STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem_w));
+      int per_sm = 1;
+      STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32,
+                                                                    smem_w));
+      const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps),
+                                             (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
+      call.before_launch("mttkrp_sparse");
+      kern<<<(unsigned)grid, kSpWarps * 32, smem_w, call.stream()>>>(P);
+      call.after_launch();
+    };
+    switch (W) {
+      case 1: launch(mttkrp_sparse_kernel<1>); break;
+      case 2: launch(mttkrp_sparse_kernel<2>); break;
+      case 4: launch(mttkrp_sparse_kernel<4>); break;
+      case 8: launch(mttkrp_sparse_kernel<8>); break;
+      default: launch(mttkrp_sparse_kernel<0>); break;
+    }
     size_t temp_bytes = 0;
     STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, cpos + 1, cpos + 1, I,
                                                   call.stream()));
