@@ -568,89 +568,138 @@ __device__ __forceinline__ int bm_rank(const unsigned long long (&b)[W], int r) 
   return n;
 }
 
-// sparse_slice with factor-row bitmaps: C_j ∩ D_k is a word-wise AND, a
-// matched column's value positions are popcounts, and value loads happen
-// only for matches (same arithmetic and order as sparse_slice).
+// Matches (C_j ∩ D_k columns of single-nonzero fibers) queued per warp so
+// that their value gathers and workspace updates run on full warps instead
+// of the few lanes that found a match.
+constexpr int kQ = 128;
+struct MatchQueue {
+  int64_t ci[kQ];  // position of C(j,r) in C's values
+  int64_t di[kQ];  // position of D(k,r) in D's values
+  double b[kQ];    // B(i,j,k)
+  int r[kQ];
+};
+
+// sparse_slice with factor-row bitmaps: C_j ∩ D_k is a word-wise AND and a
+// matched column's value positions are popcounts; matches are queued and
+// evaluated 32 at a time (same arithmetic and per-entry order as
+// sparse_slice: w0 = 0 + b*D(k,r), w1(r) += w0*C(j,r)).
 template <int W>
 __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, uint32_t* wb,
-                                unsigned long long& mults) {
+                                unsigned long long& mults, MatchQueue& Q) {
   const int lane = (int)lane_id();
   const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
-  for (int64_t f = f0 + lane; f < f1; f += 32) {
-    const int64_t j = P.idx1[f];
-    const int64_t z0 = P.pos2[f], z1 = P.pos2[f + 1];
-    unsigned long long bc[W];
-    load_bm<W>(P.cbm + j * W, bc);
-    if (z1 - z0 == 1) {
-      const int64_t k = P.idx2[z0];
-      const double b = P.vals[z0];
-      unsigned long long bd[W];
-      load_bm<W>(P.dbm + k * W, bd);
-      unsigned long long any = 0ull;
+  int qn = 0;  // queued matches (warp-uniform)
+  auto flush = [&]() {
+    for (int t = lane; t < qn; t += 32) {
+      const double w0 = add_rn(0.0, mul_rn(Q.b[t], P.dvals[Q.di[t]]));
+      ws_add(wv, wb, Q.r[t], mul_rn(w0, P.cvals[Q.ci[t]]));
+    }
+    __syncwarp();
+    qn = 0;
+  };
+  for (int64_t fb = f0; fb < f1; fb += 32) {
+    const int64_t f = fb + lane;
+    int nm = 0;
+    int64_t j = 0, k = 0;
+    double b = 0.0;
+    unsigned long long m[W];
+    unsigned long long bc[W], bd[W];
 #pragma unroll
-      for (int w = 0; w < W; w++) {
-        mults += (unsigned long long)__popcll(bd[w]);
-        any |= bc[w] & bd[w];
-      }
-      if (any) {
-        const int64_t c0 = P.cpos[j], d0 = P.dpos[k];
-        int rc = 0, rd = 0;
-#pragma unroll
-        for (int w = 0; w < W; w++) {
-          unsigned long long m = bc[w] & bd[w];
-          while (m) {
-            const int bit = __ffsll((long long)m) - 1;
-            const unsigned long long below = (1ull << bit) - 1ull;
-            const int ic = rc + __popcll(bc[w] & below);
-            const int id = rd + __popcll(bd[w] & below);
-            // w0(r) = 0 + b*D(k,r);  w1(r) += w0(r)*C(j,r)
-            const double w0 = add_rn(0.0, mul_rn(b, P.dvals[d0 + id]));
-            ws_add(wv, wb, w * 64 + bit, mul_rn(w0, P.cvals[c0 + ic]));
-            mults++;
-            m &= m - 1ull;
-          }
-          rc += __popcll(bc[w]);
-          rd += __popcll(bd[w]);
-        }
-      }
-    } else {
-      // general fiber: w0 at each of C_j's columns, accumulated over k in order
-      for (int64_t z = z0; z < z1; z++) {
-        const int64_t k = P.idx2[z];
-        unsigned long long bd[W];
+    for (int w = 0; w < W; w++) m[w] = bc[w] = bd[w] = 0ull;
+    bool single = false;
+    if (f < f1) {
+      j = P.idx1[f];
+      const int64_t z0 = P.pos2[f], z1 = P.pos2[f + 1];
+      load_bm<W>(P.cbm + j * W, bc);
+      if (z1 - z0 == 1) {
+        single = true;
+        k = P.idx2[z0];
+        b = P.vals[z0];
         load_bm<W>(P.dbm + k * W, bd);
 #pragma unroll
-        for (int w = 0; w < W; w++) mults += (unsigned long long)__popcll(bd[w]);
-      }
-      const int64_t c0 = P.cpos[j];
-      int ic = 0;
+        for (int w = 0; w < W; w++) {
+          mults += (unsigned long long)__popcll(bd[w]);
+          m[w] = bc[w] & bd[w];
+          nm += __popcll(m[w]);
+        }
+      } else {
+        // general fiber: w0 at each of C_j's columns, accumulated over k in order
+        for (int64_t z = z0; z < z1; z++) {
+          unsigned long long bz[W];
+          load_bm<W>(P.dbm + P.idx2[z] * W, bz);
 #pragma unroll
-      for (int w = 0; w < W; w++) {
-        unsigned long long m = bc[w];
-        while (m) {
-          const int bit = __ffsll((long long)m) - 1;
-          const int r = w * 64 + bit;
-          double w0 = 0.0;
-          bool present = false;
-          for (int64_t z = z0; z < z1; z++) {
-            const int64_t k = P.idx2[z];
-            unsigned long long bd[W];
-            load_bm<W>(P.dbm + k * W, bd);
-            if ((bd[w] >> bit) & 1ull) {
-              w0 = add_rn(w0, mul_rn(P.vals[z], P.dvals[P.dpos[k] + bm_rank<W>(bd, r)]));
-              present = true;
+          for (int w = 0; w < W; w++) mults += (unsigned long long)__popcll(bz[w]);
+        }
+        const int64_t c0 = P.cpos[j];
+        int ic = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          unsigned long long cm = bc[w];
+          while (cm) {
+            const int bit = __ffsll((long long)cm) - 1;
+            const int r = w * 64 + bit;
+            double w0 = 0.0;
+            bool present = false;
+            for (int64_t z = z0; z < z1; z++) {
+              const int64_t kz = P.idx2[z];
+              unsigned long long bz[W];
+              load_bm<W>(P.dbm + kz * W, bz);
+              if ((bz[w] >> bit) & 1ull) {
+                w0 = add_rn(w0, mul_rn(P.vals[z], P.dvals[P.dpos[kz] + bm_rank<W>(bz, r)]));
+                present = true;
+              }
             }
+            if (present) {
+              ws_add(wv, wb, r, mul_rn(w0, P.cvals[c0 + ic]));
+              mults++;
+            }
+            ic++;
+            cm &= cm - 1ull;
           }
-          if (present) {
-            ws_add(wv, wb, r, mul_rn(w0, P.cvals[c0 + ic]));
-            mults++;
-          }
-          ic++;
-          m &= m - 1ull;
         }
       }
     }
+    const int inc = warp_inclusive_scan(nm);
+    const int tot = __shfl_sync(kFull, inc, 31);
+    if (tot == 0) continue;
+    if (tot > kQ - qn) flush();
+    const bool direct = tot > kQ;  // more matches than the queue holds: per lane
+    if (single && nm > 0) {
+      const int64_t c0 = P.cpos[j], d0 = P.dpos[k];
+      int slot = qn + inc - nm;
+      int rc = 0, rd = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        unsigned long long mm = m[w];
+        while (mm) {
+          const int bit = __ffsll((long long)mm) - 1;
+          const unsigned long long below = (1ull << bit) - 1ull;
+          const int64_t ci = c0 + rc + __popcll(bc[w] & below);
+          const int64_t di = d0 + rd + __popcll(bd[w] & below);
+          if (direct) {
+            const double w0 = add_rn(0.0, mul_rn(b, P.dvals[di]));
+            ws_add(wv, wb, w * 64 + bit, mul_rn(w0, P.cvals[ci]));
+          } else {
+            Q.ci[slot] = ci;
+            Q.di[slot] = di;
+            Q.b[slot] = b;
+            Q.r[slot] = w * 64 + bit;
+            slot++;
+          }
+          mults++;
+          mm &= mm - 1ull;
+        }
+        rc += __popcll(bc[w]);
+        rd += __popcll(bd[w]);
+      }
+    }
+    __syncwarp();
+    if (!direct) {
+      qn += tot;
+      if (qn >= kQ - 32) flush();
+    }
   }
+  flush();
 }
 
 // Each warp claims slices dynamically, evaluates one into its shared-memory
@@ -658,8 +707,11 @@ __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, ui
 // holds at most R entries), recording the count in the row-pointer array.  No
 // ordering between slices is needed here; a scan and a coalesced compaction
 // copy build the CSR afterwards (no look-back waits on slower slices).
+#ifndef SP_MINB
+#define SP_MINB 4  // resident CTAs per SM the register budget targets
+#endif
 template <int W>
-__global__ void __launch_bounds__(kSpWarps * 32, 5) mttkrp_sparse_kernel(const SparseParams P) {
+__global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(const SparseParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
@@ -668,6 +720,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, 5) mttkrp_sparse_kernel(const S
   const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
   double* wv = reinterpret_cast<double*>(smem_raw + (size_t)warp * ws_bytes);
   uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
+  MatchQueue* queues = reinterpret_cast<MatchQueue*>(smem_raw + (size_t)kSpWarps * ws_bytes);
   unsigned long long mults = 0;
   while (true) {
     int64_t i = 0;
@@ -678,7 +731,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, 5) mttkrp_sparse_kernel(const S
     for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
     __syncwarp();
     if constexpr (W > 0)
-      sparse_slice_bm<W>(P, i, wv, wb, mults);
+      sparse_slice_bm<W>(P, i, wv, wb, mults, queues[warp]);
     else
       sparse_slice(P, i, wv, wb, mults);
     __syncwarp();
@@ -810,7 +863,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     if (Cv->ncols != Dv->ncols) fail(STAM_ERR_DIMENSION_MISMATCH, "mttkrp: C and D ranks differ");
     const int64_t I = B->dims[0], R = Cv->ncols;
     const size_t ws_bytes = (((size_t)R * 8 + (size_t)((R + 31) / 32) * 4) + 15) & ~(size_t)15;
-    const size_t smem = ws_bytes * kSpWarps;
+    const size_t smem = ws_bytes * kSpWarps + sizeof(MatchQueue) * kSpWarps;
     if (smem > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "sparse mttkrp: rank too large for the shared-memory "
                                        "row workspace in ABI v1 (R <= ~1700)");
@@ -830,7 +883,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.dpos = call.device_input(Dv->pos, (size_t)Dv->nrows + 1, Dv->mem);
     P.didx = call.device_input(Dv->idx, (size_t)Dv->nnz, Dv->mem);
     P.dvals = call.device_input(Dv->vals, (size_t)Dv->nnz, Dv->mem);
-    const size_t smem_w = ws_bytes * kSpWarps;
+    const size_t smem_w = ws_bytes * kSpWarps + sizeof(MatchQueue) * kSpWarps;
     P.stage_idx = call.scratch_n<int64_t>((size_t)(I * R));
     P.stage_vals = call.scratch_n<double>((size_t)(I * R));
     auto* ctl = static_cast<uint64_t*>(call.scratch_zero(4 * 8));
