@@ -428,8 +428,10 @@ __device__ __forceinline__ int hash_insert(uint32_t* keys, uint32_t key, int slo
 }
 
 // A row with P products uses tb = next_pow2(2P) main slots (at least 64) and
-// tb/2 overflow slots: at most P <= tb/2 entries are inserted, so forward
-// probing never runs off the end.
+// tb/2 overflow slots: at most P <= tb/2 entries are inserted, all at or after
+// their home slot (< tb), so forward probing never runs off the end (a load
+// of at most 1/2 keeps the order-preserving runs short).  TB is the tier's
+// largest tb.
 template <int TB>
 struct HashSmem {
   uint32_t keys[TB + TB / 2];
@@ -561,11 +563,18 @@ __device__ void drain_table(const uint32_t* keys, const double* vals, int nslots
         e += 32;
       }
       const int len = e - c;
+      // dense columns land in order (no collisions): emit directly
+      bool disorder = false;
+      for (int x = lane; x + 1 < len; x += 32) disorder |= keys[c + x] > keys[c + x + 1];
+      const bool sorted = !__any_sync(kFull, disorder);
       for (int x = lane; x < len + (32 - len % 32) % 32; x += 32) {
         const bool mine = x < len;
         const uint32_t kx = mine ? keys[c + x] : kEmpty;
-        int rank = 0;
-        for (int j = 0; j < len; j++) rank += keys[c + j] < kx ? 1 : 0;
+        int rank = x;
+        if (!sorted) {
+          rank = 0;
+          for (int j = 0; j < len; j++) rank += keys[c + j] < kx ? 1 : 0;
+        }
         if (mine) {
           out_idx[base + rank] = c0 + (int64_t)kx;
           out_vals[base + rank] = vals[c + x];

@@ -73,8 +73,8 @@ def test_spgemm_rectangular_and_empty_rows(ctx):
 
 
 def test_spgemm_every_bin_boundary(ctx):
-    # rows with exactly 32/33/256/257/1024/1025/4096/4097 products
-    targets = [0, 1, 32, 33, 256, 257, 1024, 1025, 4096, 4097, 20000]
+    # rows with exactly the tier-boundary product counts (and one past each)
+    targets = [0, 1, 32, 33, 64, 65, 256, 257, 1024, 1025, 2048, 2049, 4096, 4097, 8192, 8193, 20000]
     n = 200_000
     B = G.csr_fixed(n // 4, n, 1, 11)  # every B row has one entry
     pos = np.zeros(len(targets) + 1, dtype=np.int64)
