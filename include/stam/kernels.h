@@ -32,9 +32,19 @@ struct ExecutionStats {
   std::string main_kernel;
 };
 
-/// C = A·B; A, B csr(); C csr() with sorted columns.
+/// C = A·B; A, B csr(); C csr() with sorted columns (o.sort = false: each
+/// row's columns in workspace order, format {dense, compressed(unordered)}).
+/// o.mode: Fused (index + values) or Assemble (exact index, zero values).
 TensorStorage spgemm(const TensorStorage& A, const TensorStorage& B, const KernelOptions& = {},
                      ExecutionStats* = nullptr);
+
+/// Compute mode (SPEC run_compute_after_assemble): the values of A·B written
+/// into `assembled`'s index, which is returned unchanged with the values;
+/// bit-identical to the CPU workspace.  Throws MissingSlot when a product's
+/// column is absent from its row.
+TensorStorage spgemmCompute(const TensorStorage& A, const TensorStorage& B,
+                            const TensorStorage& assembled, const KernelOptions& = {},
+                            ExecutionStats* = nullptr);
 
 /// D = ops[0] + ops[1] + ...; all csr() of equal dimensions.
 TensorStorage spadd(std::span<const TensorStorage* const> ops, const KernelOptions& = {},

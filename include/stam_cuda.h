@@ -141,7 +141,7 @@ typedef struct stam_dense_result {
 /* ---- options and counters ------------------------------------------------*/
 typedef struct stam_options {
   int32_t sort;       /* 1 (default): sorted coordinates per row */
-  int32_t mode;       /* enum stam_mode; only FUSED in ABI v1 for MTTKRP */
+  int32_t mode;       /* enum stam_mode: SpGEMM all three; FUSED for SpAdd/MTTKRP */
   int32_t result_mem; /* enum stam_mem for the result buffers */
   int32_t timing;     /* 1: record CUDA events around each kernel (stats) */
 } stam_options;
@@ -195,6 +195,22 @@ STAM_CUDA_API int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A,
                                    const stam_csr_view* B,
                                    const stam_options* opts,
                                    stam_csr_result* C, stam_stats* stats);
+
+/* opts->mode: FUSED (default) computes index and values; ASSEMBLE computes
+ * the exact index only (values zero; the symbolic / assembly phase,
+ * PAPER.md:1116-1146); COMPUTE is stam_cuda_spgemm_compute.  opts->sort = 0
+ * leaves each row's columns in workspace order (same set per row). */
+
+/* COMPUTE mode (SPEC run_compute_after_assemble): the
+ * values of A·B written into the pre-assembled index `Cidx` (pos/idx, e.g. an
+ * ASSEMBLE result; rows sorted unless opts->sort = 0; values ignored).  The
+ * result carries Cidx's pos/idx unchanged and every value is the canonical
+ * sequential sum (bit-identical to the CPU reference).  A product whose
+ * column is absent from its row fails with STAM_ERR_MISSING_SLOT. */
+STAM_CUDA_API int stam_cuda_spgemm_compute(stam_cuda_ctx* ctx, const stam_csr_view* A,
+                                           const stam_csr_view* B, const stam_csr_view* Cidx,
+                                           const stam_options* opts,
+                                           stam_csr_result* C, stam_stats* stats);
 
 /* D = ops[0] + ops[1] + ... , every operand row scattered into one row
  * workspace in operand order, no pairwise merge:

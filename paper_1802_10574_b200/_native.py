@@ -94,6 +94,9 @@ SIGNATURES = {
     "stam_cuda_release": (C.c_int, [C.c_void_p, C.c_void_p]),
     "stam_cuda_spgemm": (C.c_int, [C.c_void_p, C.POINTER(CsrView), C.POINTER(CsrView),
                                    C.POINTER(Options), C.POINTER(CsrResult), C.POINTER(Stats)]),
+    "stam_cuda_spgemm_compute": (C.c_int, [C.c_void_p, C.POINTER(CsrView), C.POINTER(CsrView),
+                                           C.POINTER(CsrView), C.POINTER(Options),
+                                           C.POINTER(CsrResult), C.POINTER(Stats)]),
     "stam_cuda_spadd": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(CsrView),
                                   C.POINTER(Options), C.POINTER(CsrResult), C.POINTER(Stats)]),
     "stam_cuda_mttkrp_dense": (C.c_int, [C.c_void_p, C.POINTER(Csf3View), C.POINTER(DenseView),

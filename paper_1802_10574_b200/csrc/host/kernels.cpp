@@ -88,7 +88,7 @@ void report(const stam_stats& s, ExecutionStats* out) {
   out->main_kernel = s.main_kernel;
 }
 
-TensorStorage adoptCsr(stam_cuda_ctx* ctx, stam_csr_result& r) {
+TensorStorage adoptCsr(stam_cuda_ctx* ctx, stam_csr_result& r, bool sorted = true) {
   TensorStorage::Level l0, l1;
   l1.pos.assign(r.pos, r.pos + r.nrows + 1);
   l1.idx.assign(r.idx, r.idx + r.nnz);
@@ -98,8 +98,9 @@ TensorStorage adoptCsr(stam_cuda_ctx* ctx, stam_csr_result& r) {
   std::vector<TensorStorage::Level> levels;
   levels.push_back(std::move(l0));
   levels.push_back(std::move(l1));
-  // the kernels produce sorted, valid CSR; skip the O(nnz) validation
-  return TensorStorage::fromArrays(dims, csr(), std::move(levels), std::move(vals), false);
+  // the kernels produce valid CSR; skip the O(nnz) validation
+  const TensorFormat fmt = sorted ? csr() : TensorFormat({dense(), compressed(false)});
+  return TensorStorage::fromArrays(dims, fmt, std::move(levels), std::move(vals), false);
 }
 
 }  // namespace
@@ -115,9 +116,33 @@ TensorStorage spgemm(const TensorStorage& A, const TensorStorage& B, const Kerne
   const stam_options opts = options(o);
   stam_csr_result r{};
   stam_stats st{};
+  if (o.mode == ExecutionMode::Compute)
+    fail(ErrorCode::PreconditionViolated,
+         "spgemm: compute mode needs the pre-assembled index (spgemmCompute)");
   check(stam_cuda_spgemm(ctx, &a, &b, &opts, &r, &st));
   report(st, stats);
-  return adoptCsr(ctx, r);
+  return adoptCsr(ctx, r, o.sort);
+}
+
+TensorStorage spgemmCompute(const TensorStorage& A, const TensorStorage& B,
+                            const TensorStorage& assembled, const KernelOptions& o,
+                            ExecutionStats* stats) {
+  require(A, csr(), "spgemm A");
+  require(B, csr(), "spgemm B");
+  if (assembled.format().order() != 2 || assembled.format().levelFormat(1).kind != ModeKind::Compressed)
+    fail(ErrorCode::PreconditionViolated, "spgemmCompute: the assembled index must be CSR");
+  if (A.dimensions()[1] != B.dimensions()[0])
+    fail(ErrorCode::DimensionMismatch, "spgemm: A columns != B rows");
+  stam_cuda_ctx* ctx = context(o.device);
+  const stam_csr_view a = csrView(A), b = csrView(B), c = csrView(assembled);
+  stam_options opts = options(o);
+  opts.mode = STAM_MODE_COMPUTE;
+  opts.sort = assembled.format().levelFormat(1).ordered ? 1 : 0;
+  stam_csr_result r{};
+  stam_stats st{};
+  check(stam_cuda_spgemm_compute(ctx, &a, &b, &c, &opts, &r, &st));
+  report(st, stats);
+  return adoptCsr(ctx, r, opts.sort != 0);
 }
 
 TensorStorage spadd(std::span<const TensorStorage* const> ops, const KernelOptions& o,

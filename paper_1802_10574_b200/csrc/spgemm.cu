@@ -31,6 +31,7 @@
 //    (B rows read coalesced), with 4 independent gathers in flight per lane.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -89,6 +90,8 @@ struct SpgemmParams {
   int64_t* cidx;
   double* cvals;
   int64_t* stats;            // [0] total products, [1] max products of a row
+  bool values;               // false: ASSEMBLE mode (index only)
+  bool sorted;               // false: rows in workspace (slot) order
 };
 
 // ---------------------------------------------------------------------------
@@ -248,7 +251,7 @@ __global__ void tiny_numeric_kernel(const SpgemmParams P, const int64_t* rows, i
     int64_t col;
     double val;
     bool has;
-    tiny_product<G>(P, i, valid, g, true, col, val, has);
+    tiny_product<G>(P, i, valid, g, P.values, col, val, has);
     bool lead = has;
 #pragma unroll
     for (int t = 0; t < G; t++) {
@@ -268,7 +271,7 @@ __global__ void tiny_numeric_kernel(const SpgemmParams P, const int64_t* rows, i
     if (lead) {
       const int64_t dst = P.cpos[i] + out;
       P.cidx[dst] = col;
-      P.cvals[dst] = w;
+      if (P.values) P.cvals[dst] = w;
     }
   }
 }
@@ -518,7 +521,7 @@ __device__ __forceinline__ int run_boundary(const uint32_t* keys, int s0, int ns
 // shuffles; runs of 32 or more slots rank through shared memory.
 template <int THREADS>
 __device__ void drain_table(const uint32_t* keys, const double* vals, int nslots, int64_t c0,
-                            int64_t* out_idx, double* out_vals, int* scan) {
+                            int64_t* out_idx, double* out_vals, int* scan, bool sorted) {
   constexpr int kWarpsN = THREADS / 32;
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
@@ -565,19 +568,20 @@ __device__ void drain_table(const uint32_t* keys, const double* vals, int nslots
       const int len = e - c;
       // dense columns land in order (no collisions): emit directly
       bool disorder = false;
-      for (int x = lane; x + 1 < len; x += 32) disorder |= keys[c + x] > keys[c + x + 1];
-      const bool sorted = !__any_sync(kFull, disorder);
+      if (sorted)
+        for (int x = lane; x + 1 < len; x += 32) disorder |= keys[c + x] > keys[c + x + 1];
+      const bool in_order = !__any_sync(kFull, disorder);
       for (int x = lane; x < len + (32 - len % 32) % 32; x += 32) {
         const bool mine = x < len;
         const uint32_t kx = mine ? keys[c + x] : kEmpty;
         int rank = x;
-        if (!sorted) {
+        if (!in_order) {
           rank = 0;
           for (int j = 0; j < len; j++) rank += keys[c + j] < kx ? 1 : 0;
         }
         if (mine) {
           out_idx[base + rank] = c0 + (int64_t)kx;
-          out_vals[base + rank] = vals[c + x];
+          if (vals) out_vals[base + rank] = vals[c + x];
         }
       }
       base += len;
@@ -592,7 +596,7 @@ __device__ void drain_table(const uint32_t* keys, const double* vals, int nslots
     const int re = __ffs(above) - 1;  // my run's end (an empty lane <= last)
     // ranks: only windows whose runs are out of order need the shuffle loop
     const uint32_t kprev = __shfl_up_sync(kFull, k, 1);
-    const bool dis = mine && lane > rs && kprev > k;
+    const bool dis = sorted && mine && lane > rs && kprev > k;
     int rank = lane - rs;
     if (__any_sync(kFull, dis)) {
       const int len = mine ? re - rs : 0;
@@ -607,7 +611,7 @@ __device__ void drain_table(const uint32_t* keys, const double* vals, int nslots
     if (mine) {
       const int pos = base + __popc(om & ((1u << rs) - 1)) + rank;
       out_idx[pos] = c0 + (int64_t)k;
-      out_vals[pos] = vals[s];
+      if (vals) out_vals[pos] = vals[s];
     }
     base += __popc(om & ((1u << last) - 1));
     c += last + 1;
@@ -665,17 +669,25 @@ __global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParam
     const SlotMap sm = row_slot_map(P, a0, na, total, tb, S.red);
     for (int s = threadIdx.x; s < nslots; s += THREADS) {
       S.keys[s] = kEmpty;
-      S.vals[s] = 0.0;
+      if (P.values) S.vals[s] = 0.0;
     }
     cta_sync<THREADS>();
-    for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
-      bool made;
-      const int s = hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
-      atomicAdd(&S.vals[s], v);
-    });
+    if (P.values) {
+      for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
+        bool made;
+        const int s = hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
+        atomicAdd(&S.vals[s], v);
+      });
+    } else {
+      for_products<false>(P, a0, na, total, [&](int64_t col, double) {
+        bool made;
+        hash_insert(S.keys, (uint32_t)(col - sm.c0), sm(col), made);
+      });
+    }
     cta_sync<THREADS>();
-    // sort the runs (mutually ordered) and write the row in slot order
-    drain_table<THREADS>(S.keys, S.vals, nslots, sm.c0, P.cidx + dst, P.cvals + dst, S.scan);
+    // rank the runs (mutually ordered) and write the row in column order
+    drain_table<THREADS>(S.keys, P.values ? S.vals : nullptr, nslots, sm.c0, P.cidx + dst,
+                         P.cvals + dst, S.scan, P.sorted);
     cta_sync<THREADS>();
   }
 }
@@ -741,7 +753,8 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
     const int64_t dst = P.cpos[i];
     const int64_t cnt = P.cpos[i + 1] - dst;
     for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
-    for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) P.cvals[dst + t] = 0.0;
+    if (P.values)
+      for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) P.cvals[dst + t] = 0.0;
     __syncthreads();
     const int64_t a0 = P.apos[i];
     const int na = (int)(P.apos[i + 1] - a0);
@@ -785,6 +798,7 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
       }
     }
     __syncthreads();
+    if (P.values)
     for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
       const int w = (int)(col >> 6);
       const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
@@ -837,6 +851,75 @@ void launch_tiny(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows,
   call.after_launch();
 }
 
+// ---------------------------------------------------------------------------
+// COMPUTE mode (SPEC run_compute_after_assemble): values of
+// A·B written into a pre-assembled index.  A warp per row walks the row's
+// products in the canonical order (k ascending, then B-row order), 32 at a
+// time; each product locates its column in the assembled row (binary search;
+// an unsorted index through a sorted copy and its permutation); lanes that hit
+// the same entry are combined in lane order by the lowest of them, so every
+// value is the sequential sum ((0 + p1) + p2) + ... of the CPU workspace —
+// bit-identical to the reference.  pos/idx are never modified.
+__global__ void compute_rows_kernel(const SpgemmParams P, const int64_t* ipos, const int64_t* skey,
+                                    const int64_t* perm, unsigned long long* claim, int* missing) {
+  const int lane = (int)lane_id();
+  while (true) {
+    int64_t i = 0;
+    if (lane == 0) i = (int64_t)atomicAdd(claim, 1ull);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= P.m) break;
+    const int64_t a0 = P.apos[i];
+    const int na = (int)(P.apos[i + 1] - a0);
+    const int total = (int)P.prod[i];
+    const int64_t c0 = ipos[i], cn = ipos[i + 1] - c0;
+    for (int base = 0; base < total; base += 32) {
+      const int j = base + lane;
+      long long slot = -1;
+      double v = 0.0;
+      if (j < total) {
+        const int p = entry_of(P.aoff + a0, na, j);
+        const int64_t q = P.bst[a0 + p] + (j - P.aoff[a0 + p]);
+        const int64_t col = P.bidx[q];
+        v = mul_rn(P.avals[a0 + p], P.bvals[q]);
+        int64_t lo = 0, len = cn;  // first index with skey >= col
+        while (len > 0) {
+          const int64_t h = len >> 1;
+          if (skey[c0 + lo + h] < col) {
+            lo += h + 1;
+            len -= h + 1;
+          } else {
+            len = h;
+          }
+        }
+        if (lo < cn && skey[c0 + lo] == col)
+          slot = (long long)(c0 + (perm ? perm[c0 + lo] : lo));
+        else
+          atomicOr(missing, 1);
+      }
+      const unsigned act = __ballot_sync(kFull, slot >= 0);
+      const unsigned peers = __match_any_sync(kFull, slot) & act;
+      const bool leader = slot >= 0 && __ffs(peers) - 1 == lane;
+      double w = leader ? P.cvals[slot] : 0.0;
+      for (int t = 0; t < 32; t++) {
+        const double vt = __shfl_sync(kFull, v, t);
+        if (leader && ((peers >> t) & 1u)) w = add_rn(w, vt);
+      }
+      if (leader) P.cvals[slot] = w;
+      __syncwarp();
+    }
+  }
+}
+
+// Row-local positions 0..len-1 of every index entry (values of the segmented
+// sort that orders an unsorted index).
+__global__ void local_positions_kernel(const int64_t* ipos, int64_t m, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < m;
+       i += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    const int64_t b = ipos[i], e = ipos[i + 1];
+    for (int64_t t = b + lane_id(); t < e; t += 32) out[t] = t - b;
+  }
+}
+
 // Orders the long rows longest first (greedy LPT over the dynamic claims).
 __global__ void gather_keys_kernel(const int64_t* rows, int64_t n, const int64_t* prod,
                                    uint64_t* keys) {
@@ -849,6 +932,47 @@ __global__ void gather_keys_kernel(const int64_t* rows, int64_t n, const int64_t
 
 using namespace stamrt;
 
+namespace stamgpu {
+namespace {
+// Inputs on the device, per-row products / per-entry offsets (rowprod), and
+// the control block read back: host[0..kNumBins) bin counts, host[kNumBins]
+// total products, host[kNumBins+1] max products of a row.
+void prepare(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
+             SpgemmParams& P, int64_t* host) {
+  using stamrt::ceil_div;
+  const int64_t m = A->nrows, n = B->ncols;
+  P = SpgemmParams{};
+  P.m = m;
+  P.n = n;
+  P.apos = call.device_input(A->pos, (size_t)m + 1, A->mem);
+  P.aidx = call.device_input(A->idx, (size_t)A->nnz, A->mem);
+  P.avals = call.device_input(A->vals, (size_t)A->nnz, A->mem);
+  P.bpos = call.device_input(B->pos, (size_t)B->nrows + 1, B->mem);
+  P.bidx = call.device_input(B->idx, (size_t)B->nnz, B->mem);
+  P.bvals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
+  P.prod = call.scratch_n<int64_t>((size_t)m);
+  P.aoff = call.scratch_n<int>((size_t)std::max<int64_t>(A->nnz, 1));
+  P.bst = call.scratch_n<int64_t>((size_t)std::max<int64_t>(A->nnz, 1));
+  auto* ctl = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * 16));
+  P.bins = reinterpret_cast<unsigned long long*>(ctl);
+  P.stats = ctl + kNumBins;
+  P.bin_rows = call.scratch_n<int64_t>((size_t)m);
+  P.cpos = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * ((size_t)m + 1)));
+  P.values = true;
+  P.sorted = true;
+  const int sms = call.ctx()->num_sms;
+  call.before_launch("spgemm_rowprod");
+  rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)sms * 8), 256, 0,
+                   call.stream()>>>(P);
+  call.after_launch();
+  static_assert(kNumBins + 2 <= 16, "control block");
+  call.read_scalars(ctl, 16, host);
+  if (host[kNumBins + 1] >= (int64_t)INT32_MAX)
+    stamrt::fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: a row has 2^31 or more products");
+}
+}  // namespace
+}  // namespace stamgpu
+
 extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, const stam_csr_view* B,
                                 const stam_options* opts, stam_csr_result* Cr, stam_stats* stats) {
   using namespace stamgpu;
@@ -857,37 +981,17 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     check_csr_view(A, "spgemm A");
     check_csr_view(B, "spgemm B");
     if (A->ncols != B->nrows) fail(STAM_ERR_DIMENSION_MISMATCH, "spgemm: A columns != B rows");
-    if (call.opts().mode != STAM_MODE_FUSED)
-      fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm supports fused mode only in ABI v1");
+    if (call.opts().mode == STAM_MODE_COMPUTE)
+      fail(STAM_ERR_PRECONDITION_VIOLATED,
+           "spgemm compute mode needs the pre-assembled index: use stam_cuda_spgemm_compute");
     if (B->ncols >= (int64_t)UINT32_MAX)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: B has 2^32 or more columns");
     const int64_t m = A->nrows, n = B->ncols;
-    SpgemmParams P{};
-    P.m = m;
-    P.n = n;
-    P.apos = call.device_input(A->pos, (size_t)m + 1, A->mem);
-    P.aidx = call.device_input(A->idx, (size_t)A->nnz, A->mem);
-    P.avals = call.device_input(A->vals, (size_t)A->nnz, A->mem);
-    P.bpos = call.device_input(B->pos, (size_t)B->nrows + 1, B->mem);
-    P.bidx = call.device_input(B->idx, (size_t)B->nnz, B->mem);
-    P.bvals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
-    P.prod = call.scratch_n<int64_t>((size_t)m);
-    P.aoff = call.scratch_n<int>((size_t)std::max<int64_t>(A->nnz, 1));
-    P.bst = call.scratch_n<int64_t>((size_t)std::max<int64_t>(A->nnz, 1));
-    auto* ctl = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * 16));
-    P.bins = reinterpret_cast<unsigned long long*>(ctl);
-    P.stats = ctl + kNumBins;
-    P.bin_rows = call.scratch_n<int64_t>((size_t)m);
-    P.cpos = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * ((size_t)m + 1)));
-    const int sms = call.ctx()->num_sms;
-
-    call.before_launch("spgemm_rowprod");
-    rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)sms * 8), 256, 0,
-                     call.stream()>>>(P);
-    call.after_launch();
+    SpgemmParams P;
     int64_t host[16];
-    static_assert(kNumBins + 2 <= 16, "control block");
-    call.read_scalars(ctl, 16, host);
+    prepare(call, A, B, P, host);
+    P.values = call.opts().mode == STAM_MODE_FUSED;
+    P.sorted = call.opts().sort != 0;
     unsigned long long counts[kNumBins], offsets[kNumBins];
     unsigned long long acc = 0;
     for (int b = 0; b < kNumBins; b++) {
@@ -895,9 +999,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
       offsets[b] = acc;
       if (b != kBinEmpty) acc += counts[b];
     }
-    const int64_t products = host[kNumBins], max_prod = host[kNumBins + 1];
-    if (max_prod >= (int64_t)INT32_MAX)
-      fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: a row has 2^31 or more products");
+    const int64_t products = host[kNumBins];
     if (counts[kBinLong] > 0 && long_smem_bytes(n, true) > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE,
            "spgemm: rows with more than 4096 products need a column bitmap of B's columns in "
@@ -962,7 +1064,9 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
                                     cudaMemcpyDeviceToDevice, call.stream()));
     P.cidx = Cr->idx;
     P.cvals = Cr->vals;
-    // numeric
+    if (!P.values && nnz > 0)  // ASSEMBLE: index only, values defined as zero
+      STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
+    // numeric (ASSEMBLE: the same passes without values)
     launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], true);
     launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], true);
     launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true);
@@ -981,5 +1085,78 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     st->ws_inserts = products;
     st->ws_resets = m;
     st->appends = nnz;
+  });
+}
+
+extern "C" int stam_cuda_spgemm_compute(stam_cuda_ctx* ctx, const stam_csr_view* A,
+                                        const stam_csr_view* B, const stam_csr_view* Cidx,
+                                        const stam_options* opts, stam_csr_result* Cr,
+                                        stam_stats* stats) {
+  using namespace stamgpu;
+  return guarded([&] {
+    Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
+    check_csr_view(A, "spgemm A");
+    check_csr_view(B, "spgemm B");
+    if (!Cidx) fail(STAM_ERR_PRECONDITION_VIOLATED, "spgemm compute: null pre-assembled index");
+    if (A->ncols != B->nrows) fail(STAM_ERR_DIMENSION_MISMATCH, "spgemm: A columns != B rows");
+    if (Cidx->nrows != A->nrows || Cidx->ncols != B->ncols)
+      fail(STAM_ERR_DIMENSION_MISMATCH, "spgemm compute: index dimensions != A rows x B columns");
+    if (Cidx->nnz < 0 || !Cidx->pos || (Cidx->nnz > 0 && !Cidx->idx))
+      fail(STAM_ERR_PRECONDITION_VIOLATED, "spgemm compute: incomplete pre-assembled index");
+    const int64_t m = A->nrows, n = B->ncols, nnz = Cidx->nnz;
+    SpgemmParams P;
+    int64_t host[16];
+    prepare(call, A, B, P, host);
+    const int64_t products = host[kNumBins];
+    const int64_t* ipos = call.device_input(Cidx->pos, (size_t)m + 1, Cidx->mem);
+    const int64_t* iidx = call.device_input(Cidx->idx, (size_t)nnz, Cidx->mem);
+    call.alloc_csr_result(Cr, m, n, nnz);
+    STAM_CUDA_CHECK(cudaMemcpyAsync(Cr->pos, ipos, sizeof(int64_t) * ((size_t)m + 1),
+                                    cudaMemcpyDeviceToDevice, call.stream()));
+    if (nnz > 0) {
+      STAM_CUDA_CHECK(cudaMemcpyAsync(Cr->idx, iidx, sizeof(int64_t) * (size_t)nnz,
+                                      cudaMemcpyDeviceToDevice, call.stream()));
+      STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
+    }
+    const int64_t* skey = iidx;
+    const int64_t* perm = nullptr;
+    if (!call.opts().sort && nnz > 0) {
+      // unsorted index: sort each row's columns, carrying their positions
+      auto* keys_out = call.scratch_n<int64_t>((size_t)nnz);
+      auto* pos_in = call.scratch_n<int64_t>((size_t)nnz);
+      auto* pos_out = call.scratch_n<int64_t>((size_t)nnz);
+      call.before_launch("spgemm_index_positions");
+      local_positions_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)call.ctx()->num_sms * 16),
+                               256, 0, call.stream()>>>(ipos, m, pos_in);
+      call.after_launch();
+      size_t tb = 0;
+      STAM_CUDA_CHECK(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, iidx, keys_out, pos_in, pos_out,
+                                                          nnz, m, ipos, ipos + 1, call.stream()));
+      void* tmp = call.scratch(tb);
+      call.before_launch("spgemm_index_sort");
+      STAM_CUDA_CHECK(cub::DeviceSegmentedSort::SortPairs(tmp, tb, iidx, keys_out, pos_in, pos_out,
+                                                          nnz, m, ipos, ipos + 1, call.stream()));
+      call.after_launch();
+      skey = keys_out;
+      perm = pos_out;
+    }
+    auto* flags = static_cast<int*>(call.scratch_zero(sizeof(int) * 4));
+    auto* claim = reinterpret_cast<unsigned long long*>(flags + 2);
+    P.cvals = Cr->vals;
+    call.before_launch("spgemm_compute_rows");
+    compute_rows_kernel<<<(unsigned)(call.ctx()->num_sms * 8), 256, 0, call.stream()>>>(
+        P, ipos, skey, perm, claim, flags);
+    call.after_launch();
+    int64_t missing = 0;
+    call.read_scalars(reinterpret_cast<const int64_t*>(flags), 1, &missing);
+    if ((int)missing != 0)
+      fail(STAM_ERR_MISSING_SLOT,
+           "spgemm compute: a product's column is missing from the pre-assembled index");
+    call.finish_csr_result(Cr, nnz);
+    call.finish();
+    stam_stats* st = call.stats();
+    st->mults = products;
+    st->adds = products;
+    st->ws_resets = m;
   });
 }

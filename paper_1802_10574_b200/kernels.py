@@ -128,12 +128,31 @@ class Context:
 
     # -- kernels -------------------------------------------------------------
     def spgemm(self, A: CSR, B: CSR, *, sort: bool = True, result: str = "device",
-               timing: bool = False, stats: Optional[N.Stats] = None) -> CSR:
+               timing: bool = False, stats: Optional[N.Stats] = None,
+               mode: str = "fused") -> CSR:
+        """mode "fused" (index + values) or "assemble" (exact index, zero
+        values: the symbolic phase); see spgemm_compute for "compute"."""
+        modes = {"fused": N.STAM_MODE_FUSED, "assemble": N.STAM_MODE_ASSEMBLE,
+                 "compute": N.STAM_MODE_COMPUTE}
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
-        opts = self.options(sort, result, timing)
+        opts = self.options(sort, result, timing, modes[mode])
         N.check(self._lib.stam_cuda_spgemm(self._ctx, C.byref(A.view()), C.byref(B.view()),
                                            C.byref(opts), C.byref(r), C.byref(st)))
+        return self._csr_out(r)
+
+    def spgemm_compute(self, A: CSR, B: CSR, index: CSR, *, sort: bool = True,
+                       result: str = "device", timing: bool = False,
+                       stats: Optional[N.Stats] = None) -> CSR:
+        """Values of A·B written into a pre-assembled index (e.g. an
+        ``spgemm(..., mode="assemble")`` result): SPEC's compute-after-assemble.
+        ``sort=False`` when the index rows are not sorted."""
+        r = N.CsrResult()
+        st = stats if stats is not None else N.Stats()
+        opts = self.options(sort, result, timing, N.STAM_MODE_COMPUTE)
+        N.check(self._lib.stam_cuda_spgemm_compute(
+            self._ctx, C.byref(A.view()), C.byref(B.view()), C.byref(index.view()),
+            C.byref(opts), C.byref(r), C.byref(st)))
         return self._csr_out(r)
 
     def spadd(self, ops: Sequence[CSR], *, sort: bool = True, result: str = "device",
