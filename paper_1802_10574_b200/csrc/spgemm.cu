@@ -860,14 +860,32 @@ void launch_tiny(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows,
 // the same entry are combined in lane order by the lowest of them, so every
 // value is the sequential sum ((0 + p1) + p2) + ... of the CPU workspace —
 // bit-identical to the reference.  pos/idx are never modified.
-__global__ void compute_rows_kernel(const SpgemmParams P, const int64_t* ipos, const int64_t* skey,
+__device__ __forceinline__ int64_t index_lookup(const int64_t* skey, const int64_t* perm,
+                                               int64_t c0, int64_t cn, int64_t col) {
+  int64_t lo = 0, len = cn;  // first index with skey >= col
+  while (len > 0) {
+    const int64_t h = len >> 1;
+    if (skey[c0 + lo + h] < col) {
+      lo += h + 1;
+      len -= h + 1;
+    } else {
+      len = h;
+    }
+  }
+  if (lo < cn && skey[c0 + lo] == col) return c0 + (perm ? perm[c0 + lo] : lo);
+  return -1;
+}
+
+__global__ void compute_rows_kernel(const SpgemmParams P, const int64_t* rows, int64_t nrows,
+                                    const int64_t* ipos, const int64_t* skey,
                                     const int64_t* perm, unsigned long long* claim, int* missing) {
   const int lane = (int)lane_id();
   while (true) {
-    int64_t i = 0;
-    if (lane == 0) i = (int64_t)atomicAdd(claim, 1ull);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= P.m) break;
+    int64_t r = 0;
+    if (lane == 0) r = (int64_t)atomicAdd(claim, 1ull);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= nrows) break;
+    const int64_t i = rows[r];
     const int64_t a0 = P.apos[i];
     const int na = (int)(P.apos[i + 1] - a0);
     const int total = (int)P.prod[i];
@@ -881,20 +899,8 @@ __global__ void compute_rows_kernel(const SpgemmParams P, const int64_t* ipos, c
         const int64_t q = P.bst[a0 + p] + (j - P.aoff[a0 + p]);
         const int64_t col = P.bidx[q];
         v = mul_rn(P.avals[a0 + p], P.bvals[q]);
-        int64_t lo = 0, len = cn;  // first index with skey >= col
-        while (len > 0) {
-          const int64_t h = len >> 1;
-          if (skey[c0 + lo + h] < col) {
-            lo += h + 1;
-            len -= h + 1;
-          } else {
-            len = h;
-          }
-        }
-        if (lo < cn && skey[c0 + lo] == col)
-          slot = (long long)(c0 + (perm ? perm[c0 + lo] : lo));
-        else
-          atomicOr(missing, 1);
+        slot = (long long)index_lookup(skey, perm, c0, cn, col);
+        if (slot < 0) atomicOr(missing, 1);
       }
       const unsigned act = __ballot_sync(kFull, slot >= 0);
       const unsigned peers = __match_any_sync(kFull, slot) & act;
@@ -908,6 +914,53 @@ __global__ void compute_rows_kernel(const SpgemmParams P, const int64_t* ipos, c
       __syncwarp();
     }
   }
+}
+
+// COMPUTE mode, rows with many products (one warp per row would serialise a
+// row's 10^4-10^5 products): every product is expanded in canonical order
+// into (entry, value) pairs at its flat position (CTA per row, no ordering
+// needed), a stable radix sort by entry keeps canonical order inside each
+// entry's run, and each run is summed sequentially — the same ((0 + p1) + p2)
+// + ... as the CPU workspace.
+__global__ void compute_expand_kernel(const SpgemmParams P, const int64_t* rows, int64_t nrows,
+                                      const int64_t* poff, const int64_t* ipos,
+                                      const int64_t* skey, const int64_t* perm,
+                                      unsigned long long* keys, double* vals, int* missing) {
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int64_t a0 = P.apos[i];
+    const int na = (int)(P.apos[i + 1] - a0);
+    const int total = (int)P.prod[i];
+    const int64_t c0 = ipos[i], cn = ipos[i + 1] - c0;
+    const int64_t o = poff[r];
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      const int p = entry_of(P.aoff + a0, na, j);
+      const int64_t q = P.bst[a0 + p] + (j - P.aoff[a0 + p]);
+      const int64_t col = P.bidx[q];
+      const int64_t e = index_lookup(skey, perm, c0, cn, col);
+      if (e < 0) atomicOr(missing, 1);
+      keys[o + j] = e < 0 ? 0ull : (unsigned long long)e;
+      vals[o + j] = mul_rn(P.avals[a0 + p], P.bvals[q]);
+    }
+  }
+}
+
+__global__ void compute_reduce_runs_kernel(const unsigned long long* keys, const double* vals,
+                                           int64_t n, double* out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[t];
+    if (t > 0 && keys[t - 1] == k) continue;
+    double w = add_rn(0.0, vals[t]);  // first insert accumulates into 0.0
+    for (int64_t u = t + 1; u < n && keys[u] == k; u++) w = add_rn(w, vals[u]);
+    out[k] = w;
+  }
+}
+
+__global__ void gather_prod_kernel(const int64_t* rows, int64_t n, const int64_t* prod,
+                                   int64_t* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = prod[rows[t]];
 }
 
 // Row-local positions 0..len-1 of every index entry (values of the segmented
@@ -970,6 +1023,24 @@ void prepare(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
   if (host[kNumBins + 1] >= (int64_t)INT32_MAX)
     stamrt::fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: a row has 2^31 or more products");
 }
+
+// Groups the rows by bin (P.bin_rows, bin b at offsets[b]; empty rows left out).
+void bin_rows(stamrt::Call& call, SpgemmParams& P, const int64_t* host,
+              unsigned long long* counts, unsigned long long* offsets) {
+  unsigned long long acc = 0;
+  for (int b = 0; b < kNumBins; b++) {
+    counts[b] = (unsigned long long)host[b];
+    offsets[b] = acc;
+    if (b != kBinEmpty) acc += counts[b];
+  }
+  auto* d_off = static_cast<unsigned long long*>(call.scratch(sizeof(unsigned long long) * kNumBins));
+  STAM_CUDA_CHECK(cudaMemcpyAsync(d_off, offsets, sizeof(unsigned long long) * kNumBins,
+                                  cudaMemcpyHostToDevice, call.stream()));
+  STAM_CUDA_CHECK(cudaMemsetAsync(P.bins, 0, sizeof(unsigned long long) * kNumBins, call.stream()));
+  call.before_launch("spgemm_bin_scatter");
+  bin_scatter_kernel<<<(unsigned)stamrt::ceil_div(P.m, 256), 256, 0, call.stream()>>>(P, d_off);
+  call.after_launch();
+}
 }  // namespace
 }  // namespace stamgpu
 
@@ -992,25 +1063,13 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     prepare(call, A, B, P, host);
     P.values = call.opts().mode == STAM_MODE_FUSED;
     P.sorted = call.opts().sort != 0;
-    unsigned long long counts[kNumBins], offsets[kNumBins];
-    unsigned long long acc = 0;
-    for (int b = 0; b < kNumBins; b++) {
-      counts[b] = (unsigned long long)host[b];
-      offsets[b] = acc;
-      if (b != kBinEmpty) acc += counts[b];
-    }
     const int64_t products = host[kNumBins];
-    if (counts[kBinLong] > 0 && long_smem_bytes(n, true) > call.ctx()->smem_optin)
+    if (host[kBinLong] > 0 && long_smem_bytes(n, true) > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE,
            "spgemm: rows with more than 4096 products need a column bitmap of B's columns in "
            "shared memory (at most ~1.2M columns in ABI v1)");
-    auto* d_off = static_cast<unsigned long long*>(call.scratch(sizeof(offsets)));
-    STAM_CUDA_CHECK(cudaMemcpyAsync(d_off, offsets, sizeof(offsets), cudaMemcpyHostToDevice,
-                                    call.stream()));
-    STAM_CUDA_CHECK(cudaMemsetAsync(P.bins, 0, sizeof(unsigned long long) * kNumBins, call.stream()));
-    call.before_launch("spgemm_bin_scatter");
-    bin_scatter_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, call.stream()>>>(P, d_off);
-    call.after_launch();
+    unsigned long long counts[kNumBins], offsets[kNumBins];
+    bin_rows(call, P, host, counts, offsets);
 
     const int64_t* rows_b[kNumBins];
     for (int b = 0; b < kNumBins; b++) rows_b[b] = P.bin_rows + offsets[b];
@@ -1143,10 +1202,60 @@ extern "C" int stam_cuda_spgemm_compute(stam_cuda_ctx* ctx, const stam_csr_view*
     auto* flags = static_cast<int*>(call.scratch_zero(sizeof(int) * 4));
     auto* claim = reinterpret_cast<unsigned long long*>(flags + 2);
     P.cvals = Cr->vals;
-    call.before_launch("spgemm_compute_rows");
-    compute_rows_kernel<<<(unsigned)(call.ctx()->num_sms * 8), 256, 0, call.stream()>>>(
-        P, ipos, skey, perm, claim, flags);
-    call.after_launch();
+    unsigned long long counts[kNumBins], offsets[kNumBins];
+    bin_rows(call, P, host, counts, offsets);
+    // rows up to the hash tiers: a warp per row; long rows: expand-sort-reduce
+    const int64_t nshort = (int64_t)offsets[kBinLong];
+    const int64_t nlong = (int64_t)counts[kBinLong];
+    if (nshort > 0) {
+      call.before_launch("spgemm_compute_rows");
+      compute_rows_kernel<<<(unsigned)(call.ctx()->num_sms * 8), 256, 0, call.stream()>>>(
+          P, P.bin_rows, nshort, ipos, skey, perm, claim, flags);
+      call.after_launch();
+    }
+    if (nlong > 0) {
+      const int64_t* lrows = P.bin_rows + offsets[kBinLong];
+      auto* poff = call.scratch_n<int64_t>((size_t)nlong + 1);
+      call.before_launch("spgemm_compute_gather");
+      gather_prod_kernel<<<(unsigned)ceil_div(nlong, 256), 256, 0, call.stream()>>>(lrows, nlong,
+                                                                                    P.prod, poff);
+      call.after_launch();
+      size_t sb = 0;
+      STAM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, sb, poff, poff, nlong + 1, call.stream()));
+      void* stmp = call.scratch(sb);
+      STAM_CUDA_CHECK(cudaMemsetAsync(poff + nlong, 0, sizeof(int64_t), call.stream()));
+      call.before_launch("spgemm_compute_scan");
+      STAM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(stmp, sb, poff, poff, nlong + 1, call.stream()));
+      call.after_launch();
+      const int64_t nexp = call.read_scalar(poff + nlong);
+      auto* k0 = call.scratch_n<unsigned long long>((size_t)nexp);
+      auto* k1 = call.scratch_n<unsigned long long>((size_t)nexp);
+      auto* v0 = call.scratch_n<double>((size_t)nexp);
+      auto* v1 = call.scratch_n<double>((size_t)nexp);
+      call.before_launch("spgemm_compute_expand");
+      compute_expand_kernel<<<(unsigned)std::min<int64_t>(nlong, (int64_t)call.ctx()->num_sms * 4),
+                              512, 0, call.stream()>>>(P, lrows, nlong, poff, ipos, skey, perm, k0,
+                                                       v0, flags);
+      call.after_launch();
+      int end_bit = 1;
+      while (end_bit < 64 && ((int64_t)1 << end_bit) < nnz) end_bit++;
+      cub::DoubleBuffer<unsigned long long> kb(k0, k1);
+      cub::DoubleBuffer<double> vb(v0, v1);
+      size_t rb = 0;
+      STAM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, rb, kb, vb, nexp, 0, end_bit,
+                                                      call.stream()));
+      void* rtmp = call.scratch(rb);
+      call.before_launch("spgemm_compute_sort");
+      STAM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(rtmp, rb, kb, vb, nexp, 0, end_bit,
+                                                      call.stream()));
+      call.after_launch();
+      call.before_launch("spgemm_compute_reduce");
+      compute_reduce_runs_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nexp, 256),
+                                                               (int64_t)call.ctx()->num_sms * 16),
+                                   256, 0, call.stream()>>>(kb.Current(), vb.Current(), nexp,
+                                                            Cr->vals);
+      call.after_launch();
+    }
     int64_t missing = 0;
     call.read_scalars(reinterpret_cast<const int64_t*>(flags), 1, &missing);
     if ((int)missing != 0)
