@@ -46,9 +46,17 @@ TensorStorage spgemmCompute(const TensorStorage& A, const TensorStorage& B,
                             const TensorStorage& assembled, const KernelOptions& = {},
                             ExecutionStats* = nullptr);
 
-/// D = ops[0] + ops[1] + ...; all csr() of equal dimensions.
+/// D = ops[0] + ops[1] + ...; all csr() of equal dimensions.  o.mode: Fused
+/// or Assemble (exact union index, zero values).
 TensorStorage spadd(std::span<const TensorStorage* const> ops, const KernelOptions& = {},
                     ExecutionStats* = nullptr);
+
+/// Compute mode: the operands' values written into `assembled`'s index in
+/// operand order (bit-identical to the workspace); MissingSlot when an
+/// operand column is absent from its row.
+TensorStorage spaddCompute(std::span<const TensorStorage* const> ops,
+                           const TensorStorage& assembled, const KernelOptions& = {},
+                           ExecutionStats* = nullptr);
 
 /// A(i,r) = sum_{j,k} B(i,j,k) D(k,r) C(j,r); B csf(3).  Dense factors
 /// (denseFormat(2)) give a dense A; csr() factors give a csr() A.

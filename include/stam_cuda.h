@@ -141,7 +141,7 @@ typedef struct stam_dense_result {
 /* ---- options and counters ------------------------------------------------*/
 typedef struct stam_options {
   int32_t sort;       /* 1 (default): sorted coordinates per row */
-  int32_t mode;       /* enum stam_mode: SpGEMM all three; FUSED for SpAdd/MTTKRP */
+  int32_t mode;       /* enum stam_mode: FUSED / ASSEMBLE (SpGEMM, SpAdd); COMPUTE via *_compute */
   int32_t result_mem; /* enum stam_mem for the result buffers */
   int32_t timing;     /* 1: record CUDA events around each kernel (stats) */
 } stam_options;
@@ -221,6 +221,18 @@ STAM_CUDA_API int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops,
                                   const stam_csr_view* ops,
                                   const stam_options* opts, stam_csr_result* D,
                                   stam_stats* stats);
+
+/* opts->mode: FUSED or ASSEMBLE (exact union index, zero values; no value
+ * traffic).  Rows come out sorted either way (a valid sort = 0 order). */
+
+/* COMPUTE mode for SpAdd: operand values written into the pre-assembled
+ * index `Didx` (sorted rows unless opts->sort = 0) in operand order (operand 0
+ * assigns, later operands accumulate) — bit-identical to the workspace.  An
+ * operand column absent from its row fails with STAM_ERR_MISSING_SLOT. */
+STAM_CUDA_API int stam_cuda_spadd_compute(stam_cuda_ctx* ctx, int32_t nops,
+                                          const stam_csr_view* ops, const stam_csr_view* Didx,
+                                          const stam_options* opts, stam_csr_result* D,
+                                          stam_stats* stats);
 
 /* A(i,r) = sum_{j,k} B(i,j,k)·D(k,r)·C(j,r), dense factors, dense A:
  *   forall(i,j) ((forall(r) A(i,r) += w0(r)*C(j,r)) where

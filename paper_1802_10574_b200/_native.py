@@ -99,6 +99,9 @@ SIGNATURES = {
                                            C.POINTER(CsrResult), C.POINTER(Stats)]),
     "stam_cuda_spadd": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(CsrView),
                                   C.POINTER(Options), C.POINTER(CsrResult), C.POINTER(Stats)]),
+    "stam_cuda_spadd_compute": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(CsrView),
+                                          C.POINTER(CsrView), C.POINTER(Options),
+                                          C.POINTER(CsrResult), C.POINTER(Stats)]),
     "stam_cuda_mttkrp_dense": (C.c_int, [C.c_void_p, C.POINTER(Csf3View), C.POINTER(DenseView),
                                          C.POINTER(DenseView), C.POINTER(Options),
                                          C.POINTER(DenseResult), C.POINTER(Stats)]),

@@ -155,6 +155,9 @@ TensorStorage spadd(std::span<const TensorStorage* const> ops, const KernelOptio
       fail(ErrorCode::DimensionMismatch, "spadd operands must have equal dimensions");
     views.push_back(csrView(*t));
   }
+  if (o.mode == ExecutionMode::Compute)
+    fail(ErrorCode::PreconditionViolated,
+         "spadd: compute mode needs the pre-assembled index (spaddCompute)");
   stam_cuda_ctx* ctx = context(o.device);
   const stam_options opts = options(o);
   stam_csr_result r{};
@@ -162,6 +165,31 @@ TensorStorage spadd(std::span<const TensorStorage* const> ops, const KernelOptio
   check(stam_cuda_spadd(ctx, (int32_t)views.size(), views.data(), &opts, &r, &st));
   report(st, stats);
   return adoptCsr(ctx, r);
+}
+
+TensorStorage spaddCompute(std::span<const TensorStorage* const> ops,
+                           const TensorStorage& assembled, const KernelOptions& o,
+                           ExecutionStats* stats) {
+  if (ops.size() < 2) fail(ErrorCode::ArityMismatch, "spadd needs at least two operands");
+  std::vector<stam_csr_view> views;
+  for (const TensorStorage* t : ops) {
+    require(*t, csr(), "spadd operand");
+    if (t->dimensions() != ops[0]->dimensions())
+      fail(ErrorCode::DimensionMismatch, "spadd operands must have equal dimensions");
+    views.push_back(csrView(*t));
+  }
+  if (assembled.format().order() != 2 || assembled.format().levelFormat(1).kind != ModeKind::Compressed)
+    fail(ErrorCode::PreconditionViolated, "spaddCompute: the assembled index must be CSR");
+  stam_cuda_ctx* ctx = context(o.device);
+  const stam_csr_view idx = csrView(assembled);
+  stam_options opts = options(o);
+  opts.mode = STAM_MODE_COMPUTE;
+  opts.sort = assembled.format().levelFormat(1).ordered ? 1 : 0;
+  stam_csr_result r{};
+  stam_stats st{};
+  check(stam_cuda_spadd_compute(ctx, (int32_t)views.size(), views.data(), &idx, &opts, &r, &st));
+  report(st, stats);
+  return adoptCsr(ctx, r, opts.sort != 0);
 }
 
 TensorStorage mttkrp(const TensorStorage& B, const TensorStorage& C, const TensorStorage& D,

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "index.cuh"
 #include "runtime.h"
 
 namespace stamgpu {
@@ -56,6 +57,7 @@ struct SpaddParams {
   uint64_t* tile_status;
   unsigned long long* tile_counter;
   int64_t* deferred_rows;
+  bool values;  // false: ASSEMBLE mode (index only, values written as zero)
   unsigned long long* deferred_count;
   int64_t* total_nnz;
 };
@@ -171,7 +173,7 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int ou
     const int len = W.seg_len[o];
     const int co = W.seg_co[o];
     for (int t = lane; t < len; t += 32) {
-      const double v = ldg_stream(vsrc + t);
+      const double v = P.values ? ldg_stream(vsrc + t) : 0.0;
       const ColT x = W.in_col[co + t];
       int m = t;
       for (int q = 0; q < nops; q++) {
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(kLongThreads) spadd_long_rows_kernel(const Spa
           const int64_t c = col - c0;
           const int w = (int)(c >> 5);
           const int rank = wpre[w] + __popc(bits[w] & ((1u << (c & 31)) - 1u));
-          const double v = __ldg(P.vals[p] + t);
+          const double v = P.values ? __ldg(P.vals[p] + t) : 0.0;
           P.out_idx[dst + rank] = col;
           P.out_vals[dst + rank] = (p == 0) ? v : add_rn(P.out_vals[dst + rank], v);
         }
@@ -481,6 +483,34 @@ void launch_tiles(stamrt::Call& call, const SpaddParams& P, int64_t ntiles) {
   call.after_launch();
 }
 
+// COMPUTE mode (SPEC run_compute_after_assemble): operand values written into
+// a pre-assembled index, a warp per row, operands in order (operand 0
+// assigns, later operands accumulate; an entry first reached by a later
+// operand accumulates into 0.0) — the workspace sequence, bit-identical.
+__global__ void spadd_compute_rows_kernel(const SpaddParams P, const int64_t* ipos,
+                                          const int64_t* skey, const int64_t* perm,
+                                          int* missing) {
+  const int lane = (int)lane_id();
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < P.nrows; i += nwarps) {
+    const int64_t c0 = ipos[i], cn = ipos[i + 1] - c0;
+    for (int o = 0; o < P.nops; o++) {
+      const int64_t b = P.pos[o][i], e = P.pos[o][i + 1];
+      for (int64_t t = b + lane; t < e; t += 32) {
+        const int64_t slot = index_lookup(skey, perm, c0, cn, __ldg(P.idx[o] + t));
+        const double v = __ldg(P.vals[o] + t);
+        if (slot < 0) {
+          atomicOr(missing, 1);
+        } else {
+          P.out_vals[slot] = o == 0 ? v : add_rn(P.out_vals[slot], v);
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 }  // namespace
 }  // namespace stamgpu
 
@@ -500,13 +530,15 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
       if (ops[p].nrows != ops[0].nrows || ops[p].ncols != ops[0].ncols)
         fail(STAM_ERR_DIMENSION_MISMATCH, "spadd operands must have equal dimensions");
     }
-    if (call.opts().mode != STAM_MODE_FUSED)
-      fail(STAM_ERR_UNSUPPORTED_MERGE, "spadd supports fused mode only in ABI v1");
+    if (call.opts().mode == STAM_MODE_COMPUTE)
+      fail(STAM_ERR_PRECONDITION_VIOLATED,
+           "spadd compute mode needs the pre-assembled index: use stam_cuda_spadd_compute");
     const int64_t nrows = ops[0].nrows, ncols = ops[0].ncols;
     SpaddParams P{};
     P.nops = nops;
     P.nrows = nrows;
     P.ntiles = ceil_div(nrows, kTileRows);
+    P.values = call.opts().mode == STAM_MODE_FUSED;
     int64_t cap = 0, accum = 0, in_bytes = 0;
     bool host_in = false;
     for (int p = 0; p < nops; p++) {
@@ -571,8 +603,9 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
           const int64_t e0 = hpos[p][r0], e1 = hpos[p][r1];
           call.copy_range(const_cast<int64_t*>(P.idx[p]) + e0, ops[p].idx + e0,
                           (size_t)(e1 - e0) * sizeof(int64_t));
-          call.copy_range(const_cast<double*>(P.vals[p]) + e0, ops[p].vals + e0,
-                          (size_t)(e1 - e0) * sizeof(double));
+          if (P.values)
+            call.copy_range(const_cast<double*>(P.vals[p]) + e0, ops[p].vals + e0,
+                            (size_t)(e1 - e0) * sizeof(double));
         }
         call.wait(call.copy_fence());
       }
@@ -635,5 +668,65 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     st->ws_inserts = cap;
     st->ws_resets = nrows;
     st->appends = nnz;
+  });
+}
+
+extern "C" int stam_cuda_spadd_compute(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,
+                                       const stam_csr_view* Didx, const stam_options* opts,
+                                       stam_csr_result* D, stam_stats* stats) {
+  using namespace stamgpu;
+  return guarded([&] {
+    Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
+    if (!ops) fail(STAM_ERR_PRECONDITION_VIOLATED, "null operand array");
+    if (nops < 2) fail(STAM_ERR_ARITY_MISMATCH, "spadd needs at least two operands");
+    if (nops > kMaxOps)
+      fail(STAM_ERR_UNSUPPORTED_MERGE, "spadd supports at most 16 operands per call");
+    for (int p = 0; p < nops; p++) {
+      check_csr_view(&ops[p], "spadd operand");
+      if (ops[p].nrows != ops[0].nrows || ops[p].ncols != ops[0].ncols)
+        fail(STAM_ERR_DIMENSION_MISMATCH, "spadd operands must have equal dimensions");
+    }
+    if (!Didx) fail(STAM_ERR_PRECONDITION_VIOLATED, "spadd compute: null pre-assembled index");
+    if (Didx->nrows != ops[0].nrows || Didx->ncols != ops[0].ncols)
+      fail(STAM_ERR_DIMENSION_MISMATCH, "spadd compute: index dimensions != operand dimensions");
+    if (Didx->nnz < 0 || !Didx->pos || (Didx->nnz > 0 && !Didx->idx))
+      fail(STAM_ERR_PRECONDITION_VIOLATED, "spadd compute: incomplete pre-assembled index");
+    const int64_t nrows = ops[0].nrows, ncols = ops[0].ncols, nnz = Didx->nnz;
+    SpaddParams P{};
+    P.nops = nops;
+    P.nrows = nrows;
+    int64_t accum = 0;
+    for (int p = 0; p < nops; p++) {
+      P.pos[p] = call.device_input(ops[p].pos, (size_t)nrows + 1, ops[p].mem);
+      P.idx[p] = call.device_input(ops[p].idx, (size_t)ops[p].nnz, ops[p].mem);
+      P.vals[p] = call.device_input(ops[p].vals, (size_t)ops[p].nnz, ops[p].mem);
+      if (p > 0) accum += ops[p].nnz;
+    }
+    const int64_t* ipos = call.device_input(Didx->pos, (size_t)nrows + 1, Didx->mem);
+    const int64_t* iidx = call.device_input(Didx->idx, (size_t)nnz, Didx->mem);
+    call.alloc_csr_result(D, nrows, ncols, nnz);
+    STAM_CUDA_CHECK(cudaMemcpyAsync(D->pos, ipos, sizeof(int64_t) * ((size_t)nrows + 1),
+                                    cudaMemcpyDeviceToDevice, call.stream()));
+    if (nnz > 0) {
+      STAM_CUDA_CHECK(cudaMemcpyAsync(D->idx, iidx, sizeof(int64_t) * (size_t)nnz,
+                                      cudaMemcpyDeviceToDevice, call.stream()));
+      STAM_CUDA_CHECK(cudaMemsetAsync(D->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
+    }
+    const IndexSearch ix = make_index_search(call, ipos, iidx, nrows, nnz, call.opts().sort != 0);
+    P.out_vals = D->vals;
+    auto* missing = static_cast<int*>(call.scratch_zero(sizeof(int64_t)));
+    call.before_launch("spadd_compute_rows");
+    spadd_compute_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nrows, 8),
+                                                            (int64_t)call.ctx()->num_sms * 16),
+                                256, 0, call.stream()>>>(P, ipos, ix.skey, ix.perm, missing);
+    call.after_launch();
+    const int64_t miss = call.read_scalar(reinterpret_cast<const int64_t*>(missing));
+    if (miss != 0)
+      fail(STAM_ERR_MISSING_SLOT, "spadd compute: an operand column is missing from the index");
+    call.finish_csr_result(D, nnz);
+    call.finish();
+    stam_stats* st = call.stats();
+    st->adds = accum;
+    st->ws_resets = nrows;
   });
 }

@@ -31,13 +31,13 @@
 //    (B rows read coalesced), with 4 independent gathers in flight per lane.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <string>
 
 #include "common.cuh"
+#include "index.cuh"
 #include "runtime.h"
 
 namespace stamgpu {
@@ -860,22 +860,6 @@ void launch_tiny(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows,
 // the same entry are combined in lane order by the lowest of them, so every
 // value is the sequential sum ((0 + p1) + p2) + ... of the CPU workspace —
 // bit-identical to the reference.  pos/idx are never modified.
-__device__ __forceinline__ int64_t index_lookup(const int64_t* skey, const int64_t* perm,
-                                               int64_t c0, int64_t cn, int64_t col) {
-  int64_t lo = 0, len = cn;  // first index with skey >= col
-  while (len > 0) {
-    const int64_t h = len >> 1;
-    if (skey[c0 + lo + h] < col) {
-      lo += h + 1;
-      len -= h + 1;
-    } else {
-      len = h;
-    }
-  }
-  if (lo < cn && skey[c0 + lo] == col) return c0 + (perm ? perm[c0 + lo] : lo);
-  return -1;
-}
-
 __global__ void compute_rows_kernel(const SpgemmParams P, const int64_t* rows, int64_t nrows,
                                     const int64_t* ipos, const int64_t* skey,
                                     const int64_t* perm, unsigned long long* claim, int* missing) {
@@ -961,16 +945,6 @@ __global__ void gather_prod_kernel(const int64_t* rows, int64_t n, const int64_t
                                    int64_t* out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) out[t] = prod[rows[t]];
-}
-
-// Row-local positions 0..len-1 of every index entry (values of the segmented
-// sort that orders an unsorted index).
-__global__ void local_positions_kernel(const int64_t* ipos, int64_t m, int64_t* out) {
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < m;
-       i += (int64_t)gridDim.x * (blockDim.x / 32)) {
-    const int64_t b = ipos[i], e = ipos[i + 1];
-    for (int64_t t = b + lane_id(); t < e; t += 32) out[t] = t - b;
-  }
 }
 
 // Orders the long rows longest first (greedy LPT over the dynamic claims).
@@ -1177,28 +1151,9 @@ extern "C" int stam_cuda_spgemm_compute(stam_cuda_ctx* ctx, const stam_csr_view*
                                       cudaMemcpyDeviceToDevice, call.stream()));
       STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
     }
-    const int64_t* skey = iidx;
-    const int64_t* perm = nullptr;
-    if (!call.opts().sort && nnz > 0) {
-      // unsorted index: sort each row's columns, carrying their positions
-      auto* keys_out = call.scratch_n<int64_t>((size_t)nnz);
-      auto* pos_in = call.scratch_n<int64_t>((size_t)nnz);
-      auto* pos_out = call.scratch_n<int64_t>((size_t)nnz);
-      call.before_launch("spgemm_index_positions");
-      local_positions_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)call.ctx()->num_sms * 16),
-                               256, 0, call.stream()>>>(ipos, m, pos_in);
-      call.after_launch();
-      size_t tb = 0;
-      STAM_CUDA_CHECK(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, iidx, keys_out, pos_in, pos_out,
-                                                          nnz, m, ipos, ipos + 1, call.stream()));
-      void* tmp = call.scratch(tb);
-      call.before_launch("spgemm_index_sort");
-      STAM_CUDA_CHECK(cub::DeviceSegmentedSort::SortPairs(tmp, tb, iidx, keys_out, pos_in, pos_out,
-                                                          nnz, m, ipos, ipos + 1, call.stream()));
-      call.after_launch();
-      skey = keys_out;
-      perm = pos_out;
-    }
+    const IndexSearch ix = make_index_search(call, ipos, iidx, m, nnz, call.opts().sort != 0);
+    const int64_t* skey = ix.skey;
+    const int64_t* perm = ix.perm;
     auto* flags = static_cast<int*>(call.scratch_zero(sizeof(int) * 4));
     auto* claim = reinterpret_cast<unsigned long long*>(flags + 2);
     P.cvals = Cr->vals;

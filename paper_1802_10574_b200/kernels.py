@@ -132,11 +132,9 @@ class Context:
                mode: str = "fused") -> CSR:
         """mode "fused" (index + values) or "assemble" (exact index, zero
         values: the symbolic phase); see spgemm_compute for "compute"."""
-        modes = {"fused": N.STAM_MODE_FUSED, "assemble": N.STAM_MODE_ASSEMBLE,
-                 "compute": N.STAM_MODE_COMPUTE}
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
-        opts = self.options(sort, result, timing, modes[mode])
+        opts = self.options(sort, result, timing, self._MODES[mode])
         N.check(self._lib.stam_cuda_spgemm(self._ctx, C.byref(A.view()), C.byref(B.view()),
                                            C.byref(opts), C.byref(r), C.byref(st)))
         return self._csr_out(r)
@@ -155,14 +153,32 @@ class Context:
             C.byref(opts), C.byref(r), C.byref(st)))
         return self._csr_out(r)
 
+    _MODES = {"fused": N.STAM_MODE_FUSED, "assemble": N.STAM_MODE_ASSEMBLE,
+              "compute": N.STAM_MODE_COMPUTE}
+
     def spadd(self, ops: Sequence[CSR], *, sort: bool = True, result: str = "device",
-              timing: bool = False, stats: Optional[N.Stats] = None) -> CSR:
+              timing: bool = False, stats: Optional[N.Stats] = None,
+              mode: str = "fused") -> CSR:
+        """mode "fused" or "assemble" (exact union index, zero values)."""
         views = (N.CsrView * len(ops))(*[o.view() for o in ops])
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
-        opts = self.options(sort, result, timing)
+        opts = self.options(sort, result, timing, self._MODES[mode])
         N.check(self._lib.stam_cuda_spadd(self._ctx, len(ops), views, C.byref(opts), C.byref(r),
                                           C.byref(st)))
+        return self._csr_out(r)
+
+    def spadd_compute(self, ops: Sequence[CSR], index: CSR, *, sort: bool = True,
+                      result: str = "device", timing: bool = False,
+                      stats: Optional[N.Stats] = None) -> CSR:
+        """Operand values written into a pre-assembled index (compute mode)."""
+        views = (N.CsrView * len(ops))(*[o.view() for o in ops])
+        r = N.CsrResult()
+        st = stats if stats is not None else N.Stats()
+        opts = self.options(sort, result, timing, N.STAM_MODE_COMPUTE)
+        N.check(self._lib.stam_cuda_spadd_compute(self._ctx, len(ops), views,
+                                                  C.byref(index.view()), C.byref(opts),
+                                                  C.byref(r), C.byref(st)))
         return self._csr_out(r)
 
     def mttkrp(self, B: CSF3, Cf, Df, *, result: str = "device", timing: bool = False,

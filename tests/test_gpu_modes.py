@@ -104,3 +104,52 @@ def test_compute_mode_flag_on_fused_entry_is_rejected(ctx):
     with pytest.raises(StamError) as e:
         ctx.spgemm(cfg["A"], cfg["B"], mode="compute")
     assert e.value.code == "PreconditionViolated"
+
+
+# --------------------------------------------------------------------------
+# SpAdd: assemble / compute (operand order: operand 0 assigns, others
+# accumulate; an entry first reached by a later operand accumulates into 0.0)
+
+@pytest.fixture(scope="module")
+def spadd_ops():
+    rng = np.random.default_rng(5)
+    ops = []
+    for k in range(3):
+        lens = rng.integers(0, 60, size=700)
+        lens[[5, 99]] = [3000, 700]  # a deferred (long) row and a postponed one
+        pos = np.zeros(701, dtype=np.int64)
+        np.cumsum(lens, out=pos[1:])
+        ops.append(G.csr_from_lengths(700, 4000, pos, 300 + k))  # narrow: many shared columns
+    return ops, oracle.spadd(ops)
+
+
+def test_spadd_assemble_exact_index(ctx, spadd_ops):
+    ops, ref = spadd_ops
+    D = ctx.spadd([_d(o) for o in ops], mode="assemble")
+    assert np.array_equal(_np(D.pos), ref["pos"]) and np.array_equal(_np(D.idx), ref["idx"])
+    assert not np.any(_np(D.vals))
+
+
+def test_spadd_compute_after_assemble_bit_identical(ctx, spadd_ops):
+    ops, ref = spadd_ops
+    idx = ctx.spadd([_d(o) for o in ops], mode="assemble")
+    D = ctx.spadd_compute([_d(o) for o in ops], idx)
+    assert oracle.compare_csr(D, ref, exact_values=True)["bit_identical"]
+
+
+def test_spadd_compute_unsorted_index_and_missing_slot(ctx, spadd_ops):
+    ops, ref = spadd_ops
+    idx = ctx.spadd(ops, mode="assemble", result="host")
+    pos, cols = _np(idx.pos), _np(idx.idx).copy()
+    for i in range(idx.nrows):  # reverse every row: a valid unsorted index
+        cols[pos[i]:pos[i + 1]] = cols[pos[i]:pos[i + 1]][::-1]
+    rev = CSR(idx.nrows, idx.ncols, pos.copy(), cols, np.zeros(cols.shape[0]))
+    D = ctx.spadd_compute(ops, rev, sort=False, result="host")
+    oracle.compare_csr(_rows_sorted(D), ref, exact_values=True)
+    short = CSR(idx.nrows, idx.ncols, np.concatenate([[0], pos[1:] - 1]) if pos[1] > 0 else pos,
+                np.delete(_np(idx.idx), 0) if pos[1] > 0 else _np(idx.idx),
+                np.zeros(cols.shape[0] - (1 if pos[1] > 0 else 0)))
+    if pos[1] > 0:
+        with pytest.raises(StamError) as e:
+            ctx.spadd_compute(ops, short)
+        assert e.value.code == "MissingSlot"
