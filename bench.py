@@ -79,6 +79,8 @@ def _csf_bytes(b) -> int:
 class Workload:
     """Common driver: inputs on device, raw C-ABI step, e2e step, CPU ref."""
 
+    mode = "fused"  # fused | assemble | compute | unsorted (SpGEMM, SpAdd)
+
     def __init__(self, cid: int, shard: int):
         from paper_1802_10574_b200 import generators as G
 
@@ -123,13 +125,34 @@ class SpaddWork(Workload):
         self.in_bytes = sum(_csr_bytes(o) for o in self.cfg["ops"])
         self.nnz_out = None
 
+    def _index(self, views):
+        """Pre-assembled index for compute mode (assembled once, reused)."""
+        if getattr(self, "_idx", None) is None:
+            N = self.N
+            r = N.CsrResult()
+            opts = N.Options(1, N.STAM_MODE_ASSEMBLE, N.STAM_MEM_DEVICE, 0)
+            N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.dev), self.views,
+                                             C.byref(opts), C.byref(r), C.byref(N.Stats())))
+            self._idx = r
+            self._idx_view = N.CsrView(r.nrows, r.ncols, r.nnz, r.pos, r.idx, r.vals,
+                                       N.STAM_MEM_DEVICE, 0)
+        return self._idx_view
+
     def _call(self, views, result_mem, timing):
         N = self.N
         r = N.CsrResult()
         st = N.Stats()
-        opts = N.Options(1, 0, result_mem, 1 if timing else 0)
-        N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.dev), views, C.byref(opts),
-                                         C.byref(r), C.byref(st)))
+        mode = {"assemble": N.STAM_MODE_ASSEMBLE, "compute": N.STAM_MODE_COMPUTE}.get(
+            self.mode, N.STAM_MODE_FUSED)
+        opts = N.Options(0 if self.mode == "unsorted" else 1, mode, result_mem,
+                         1 if timing else 0)
+        if self.mode == "compute":
+            N.check(self.lib.stam_cuda_spadd_compute(
+                self.ctx._ctx, len(self.dev), views, C.byref(self._index(views)), C.byref(opts),
+                C.byref(r), C.byref(st)))
+        else:
+            N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.dev), views, C.byref(opts),
+                                             C.byref(r), C.byref(st)))
         nnz, nrows = r.nnz, r.nrows
         N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
         self.nnz_out = nnz
@@ -200,13 +223,34 @@ class SpgemmWork(Workload):
         self.products = int(np.sum(np.diff(B.pos)[A.idx]))
         self.nnz_out = None
 
+    def _index(self):
+        """Pre-assembled index for compute mode (assembled once, reused)."""
+        if getattr(self, "_idx", None) is None:
+            N = self.N
+            r = N.CsrResult()
+            opts = N.Options(1, N.STAM_MODE_ASSEMBLE, N.STAM_MEM_DEVICE, 0)
+            N.check(self.lib.stam_cuda_spgemm(self.ctx._ctx, C.byref(self.va), C.byref(self.vb),
+                                              C.byref(opts), C.byref(r), C.byref(N.Stats())))
+            self._idx = r
+            self._idx_view = N.CsrView(r.nrows, r.ncols, r.nnz, r.pos, r.idx, r.vals,
+                                       N.STAM_MEM_DEVICE, 0)
+        return self._idx_view
+
     def _call(self, va, vb, result_mem, timing):
         N = self.N
         r = N.CsrResult()
         st = N.Stats()
-        opts = N.Options(1, 0, result_mem, 1 if timing else 0)
-        N.check(self.lib.stam_cuda_spgemm(self.ctx._ctx, C.byref(va), C.byref(vb), C.byref(opts),
-                                          C.byref(r), C.byref(st)))
+        mode = {"assemble": N.STAM_MODE_ASSEMBLE, "compute": N.STAM_MODE_COMPUTE}.get(
+            self.mode, N.STAM_MODE_FUSED)
+        opts = N.Options(0 if self.mode == "unsorted" else 1, mode, result_mem,
+                         1 if timing else 0)
+        if self.mode == "compute":
+            N.check(self.lib.stam_cuda_spgemm_compute(self.ctx._ctx, C.byref(va), C.byref(vb),
+                                                      C.byref(self._index()), C.byref(opts),
+                                                      C.byref(r), C.byref(st)))
+        else:
+            N.check(self.lib.stam_cuda_spgemm(self.ctx._ctx, C.byref(va), C.byref(vb),
+                                              C.byref(opts), C.byref(r), C.byref(st)))
         self.nnz_out = r.nnz
         self.out_bytes = 8 * (r.nrows + 1) + 16 * r.nnz
         N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
@@ -488,6 +532,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="fused", choices=["fused", "assemble", "compute", "unsorted"],
+                    help="execution mode (SpGEMM / SpAdd configs): SPEC.md:372-374, sort flag :351")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cid = args.config
@@ -509,6 +555,10 @@ def main():
     from paper_1802_10574_b200 import Context
 
     W = WORKLOADS[cid](cid, rank)
+    if args.mode != "fused":
+        if cid not in (1, 2, 3):
+            raise SystemExit("--mode applies to the SpGEMM and SpAdd configs (1, 2, 3)")
+        W.mode = args.mode
     ctx = Context(local)
     stream = torch.cuda.Stream(device=local)
     ctx.set_stream(stream)
@@ -579,6 +629,7 @@ def main():
                        "l2": "inputs larger than L2 (no flush)" if W.in_bytes > 126e6
                        else "inputs smaller than L2",
                        "algo_bytes_per_step": algo, "nnz_out": W.nnz_out,
+                       **({"mode": W.mode} if W.mode != "fused" else {}),
                        "parallelism": f"row shards x{world} (weak)"},
             "useful_gflops": W.flops() * world / (ms_max * 1e-3) / 1e9,
             "kernel_ms": kernel_ms, "kernels_total_ms": statistics.mean(tot_ms),
