@@ -7,6 +7,11 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdio>
+#include <fstream>
+#include <string>
+
+#include "stam/io.h"
 #include "stam/kernels.h"
 #include "stam/storage.h"
 #include "stam/workspace.h"
@@ -113,6 +118,80 @@ TEST_CASE("gpu: mttkrp dense and sparse") {
   // present-checked: A(0,0)=1*1*5 ; A(0,1)=2*4*8 ; A(1,0)=3*3*5 ; A(1,1)=3*4*6
   CHECK(As.level(1).pos == std::vector<int64_t>{0, 2, 4});
   CHECK(As.vals() == std::vector<double>{5, 64, 45, 72});
+}
+
+static std::string tmpFile(const char* name, const char* text) {
+  std::string path = std::string("/tmp/stam_io_") + name;
+  std::ofstream(path) << text;
+  return path;
+}
+
+TEST_CASE("io: matrix market identity, symmetric expansion, errors") {
+  TensorStorage I = loadMatrixMarket(
+      tmpFile("id.mtx", "%%MatrixMarket matrix coordinate real general\n% c\n2 2 2\n1 1 1\n2 2 1\n"));
+  CHECK(I.format() == csr());
+  CHECK(I.level(1).pos == std::vector<int64_t>{0, 1, 2});
+  CHECK(I.level(1).idx == std::vector<int64_t>{0, 1});
+  CHECK(I.vals() == std::vector<double>{1, 1});
+  TensorStorage S = loadMatrixMarket(
+      tmpFile("sym.mtx", "%%MatrixMarket matrix coordinate real symmetric\n3 3 2\n2 1 5\n3 3 1\n"));
+  CHECK(S.storedCount() == 3);  // (2,1) expanded to (1,2)
+  CHECK(S.locate({0, 1}).has_value());
+  TensorStorage Pt = loadMatrixMarket(
+      tmpFile("pat.mtx", "%%MatrixMarket matrix coordinate pattern general\n2 3 2\n1 3\n1 3\n"));
+  CHECK(Pt.vals() == std::vector<double>{2.0});  // duplicates summed (1.0 each)
+  CHECK_THROWS_AS(loadMatrixMarket(tmpFile("bad.mtx", "%%MatrixMarket tensor coordinate real general\n")),
+                  Error);
+  CHECK_THROWS_AS(loadMatrixMarket(tmpFile("oob.mtx",
+                                           "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1\n")),
+                  Error);
+}
+
+TEST_CASE("io: tns order 3, duplicates summed, 0-based rejected, round trip") {
+  TensorStorage T = loadTns(tmpFile("t.tns", "# c\n1 1 1 1.5\n2 3 1 2\n1 1 1 0.5\n1 2 2 3\n"));
+  CHECK(T.format() == csf(3));
+  CHECK(T.storedCount() == 3);
+  CHECK(T.dimensions() == std::vector<int64_t>{2, 3, 2});
+  CHECK(*T.locate({0, 0, 0}) == 0);
+  CHECK(T.vals()[0] == 2.0);
+  CHECK_THROWS_AS(loadTns(tmpFile("z.tns", "0 1 1 1\n")), Error);
+  const std::string p = "/tmp/stam_io_rt.tns";
+  store(p, T);
+  TensorStorage U = loadTns(p, T.dimensions());
+  CHECK(U.level(1).pos == T.level(1).pos);
+  CHECK(U.level(2).idx == T.level(2).idx);
+  CHECK(U.vals() == T.vals());
+  TensorStorage A = csrOf(3, 4, {0, 2, 2, 3}, {0, 3, 1}, {0.1, -2.5e-300, 1.0 / 3.0});
+  store("/tmp/stam_io_rt.mtx", A);
+  TensorStorage B = loadMatrixMarket("/tmp/stam_io_rt.mtx");
+  CHECK(B.level(1).pos == A.level(1).pos);
+  CHECK(B.level(1).idx == A.level(1).idx);
+  CHECK(B.vals() == A.vals());  // 17 significant digits: exact
+}
+
+TEST_CASE("gpu: assemble / compute modes and unsorted output") {
+  if (!g_gpu) return;
+  TensorStorage A = csrOf(2, 2, {0, 2, 3}, {0, 1, 1}, {1, 2, 3});
+  TensorStorage B = csrOf(2, 2, {0, 1, 3}, {0, 0, 1}, {4, 5, 6});
+  KernelOptions asm_opts;
+  asm_opts.mode = ExecutionMode::Assemble;
+  TensorStorage idx = spgemm(A, B, asm_opts);
+  CHECK(idx.level(1).pos == std::vector<int64_t>{0, 2, 4});
+  CHECK(idx.vals() == std::vector<double>{0, 0, 0, 0});
+  TensorStorage C = spgemmCompute(A, B, idx);
+  CHECK(C.vals() == std::vector<double>{14, 12, 15, 18});
+  KernelOptions cmp;
+  cmp.mode = ExecutionMode::Compute;
+  CHECK_THROWS_AS(spgemm(A, B, cmp), Error);
+  KernelOptions uns;
+  uns.sort = false;
+  TensorStorage Cu = spgemm(A, B, uns);
+  CHECK(!Cu.format().levelFormat(1).ordered);
+  CHECK(Cu.storedCount() == 4);
+  const TensorStorage* ops[] = {&A, &B};
+  TensorStorage sidx = spadd(ops, asm_opts);
+  TensorStorage S = spaddCompute(ops, sidx);
+  CHECK(S.vals() == std::vector<double>{5, 2, 5, 9});
 }
 
 static int g_init = [] {

@@ -153,3 +153,23 @@ def test_spadd_compute_unsorted_index_and_missing_slot(ctx, spadd_ops):
         with pytest.raises(StamError) as e:
             ctx.spadd_compute(ops, short)
         assert e.value.code == "MissingSlot"
+
+
+# --------------------------------------------------------------------------
+# exchange formats feeding the kernels
+
+def test_loaded_files_through_the_kernels(ctx, tmp_path):
+    from paper_1802_10574_b200 import io as sio
+
+    A = G.csr_powerlaw(2000, 2000, 77, lmax=300)
+    sio.store(tmp_path / "a.mtx", A)
+    L = sio.load_matrix_market(tmp_path / "a.mtx")
+    oracle.compare_csr(ctx.spgemm(_d(L), _d(L)), oracle.spgemm(A, A))
+    B = G.csf3((50, 60, 70), G.slice_sizes_ranksize(50, 4000, 1.5, 3), 4)
+    sio.store(tmp_path / "b.tns", B)
+    T = sio.load_tns(tmp_path / "b.tns", dims=B.dims)
+    Cf, Df = G.dense(60, 32, 5), G.dense(70, 32, 6)
+    got = _np(ctx.mttkrp(T, Cf, Df).vals)
+    ref = oracle.mttkrp_dense(B, Cf.vals, Df.vals)
+    bound = 1e-12 * np.maximum(np.abs(ref["vals"]), ref["abs"])
+    assert np.all(np.abs(got - ref["vals"]) <= bound)
