@@ -395,6 +395,41 @@ class MttkrpWork(Workload):
 WORKLOADS = {1: SpgemmWork, 2: SpaddWork, 3: SpgemmWork, 4: MttkrpWork, 5: MttkrpWork}
 
 
+class FileSpgemmWork(SpgemmWork):
+    """C = A*A for a Matrix Market file (SuiteSparse-style input; --mtx)."""
+
+    def __init__(self, path: str):
+        from paper_1802_10574_b200 import io as sio
+
+        self.cid = 0
+        self.name = f"file:{Path(path).name}:AxA"
+        t = time.time()
+        A = sio.load_matrix_market(path)
+        if A.nrows != A.ncols:
+            raise SystemExit("--mtx: A*A needs a square matrix")
+        self.cfg = {"kind": "spgemm", "A": A, "B": A}
+        self.gen_s = time.time() - t
+
+
+class FileMttkrpWork(MttkrpWork):
+    """Dense-factor MTTKRP on a FROSTT .tns file (order 3; --tns), seeded
+    random factors of rank --rank."""
+
+    def __init__(self, path: str, rank: int):
+        from paper_1802_10574_b200 import generators as G
+        from paper_1802_10574_b200 import io as sio
+
+        self.cid = 0
+        self.name = f"file:{Path(path).name}:R{rank}"
+        t = time.time()
+        B = sio.load_tns(path)
+        if not hasattr(B, "pos1"):
+            raise SystemExit("--tns: an order-3 tensor is needed")
+        self.cfg = {"kind": "mttkrp_dense", "B": B, "C": G.dense(B.dims[1], rank, 401),
+                    "D": G.dense(B.dims[2], rank, 402)}
+        self.gen_s = time.time() - t
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler
 # ---------------------------------------------------------------------------
@@ -532,6 +567,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mtx", help="SpGEMM A*A on this Matrix Market file instead of a config")
+    ap.add_argument("--tns", help="dense MTTKRP on this FROSTT .tns file instead of a config")
+    ap.add_argument("--rank", type=int, default=32, help="factor rank for --tns")
     ap.add_argument("--mode", default="fused", choices=["fused", "assemble", "compute", "unsorted"],
                     help="execution mode (SpGEMM / SpAdd configs): SPEC.md:372-374, sort flag :351")
     args = ap.parse_args()
@@ -554,9 +592,14 @@ def main():
 
     from paper_1802_10574_b200 import Context
 
-    W = WORKLOADS[cid](cid, rank)
+    if args.mtx:
+        W = FileSpgemmWork(args.mtx)
+    elif args.tns:
+        W = FileMttkrpWork(args.tns, args.rank)
+    else:
+        W = WORKLOADS[cid](cid, rank)
     if args.mode != "fused":
-        if cid not in (1, 2, 3):
+        if cid not in (1, 2, 3) and not args.mtx:
             raise SystemExit("--mode applies to the SpGEMM and SpAdd configs (1, 2, 3)")
         W.mode = args.mode
     ctx = Context(local)
@@ -624,8 +667,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded; BASELINE shapes, see DESIGN.md)",
-            "config": {"workload": W.name, "config_id": cid,
+            "dtype": "f64",
+            "data": ("file " + (args.mtx or args.tns)) if W.cid == 0 else
+                    "synthetic (seeded; BASELINE shapes, see DESIGN.md)",
+            "config": {"workload": W.name, "config_id": cid if W.cid else None,
                        "l2": "inputs larger than L2 (no flush)" if W.in_bytes > 126e6
                        else "inputs smaller than L2",
                        "algo_bytes_per_step": algo, "nnz_out": W.nnz_out,
