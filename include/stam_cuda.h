@@ -259,6 +259,31 @@ STAM_CUDA_API int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx,
                                           const stam_options* opts,
                                           stam_csr_result* A, stam_stats* stats);
 
+/* ---- SPEC kernels outside the workspace plans ------------*/
+
+/* TTV (SPEC Fig. ttv: forall(i,j,k) A(i,j) += B(i,j,k)*c(k)): CSR result over
+ * B's (i,j) fibers, each value summed over k in order.  c holds dims[2]
+ * values (any dense shape). */
+STAM_CUDA_API int stam_cuda_ttv(stam_cuda_ctx* ctx, const stam_csf3_view* B,
+                                const stam_dense_view* c, const stam_options* opts,
+                                stam_csr_result* A, stam_stats* stats);
+
+/* row-dot (a(i) = sum(j) B(i,j)*C(i,j), no workspace):
+ * intersection of the sorted rows, summed in j order; a is nrows x 1.
+ * stats->merge_compares = the two-pointer loop iterations. */
+STAM_CUDA_API int stam_cuda_rowdot(stam_cuda_ctx* ctx, const stam_csr_view* B,
+                                   const stam_csr_view* C, const stam_options* opts,
+                                   stam_dense_result* a, stam_stats* stats);
+
+/* Merge-based SpAdd baseline: D = ((ops[0] + ops[1]) +
+ * ops[2]) + ..., each step a two-way union co-iteration (coinciding entries
+ * add, lone entries are copied); stats->merge_compares counts the loop
+ * iterations (one per union coordinate).  The workspace plan is
+ * stam_cuda_spadd (merge_compares == 0). */
+STAM_CUDA_API int stam_cuda_spadd_merge(stam_cuda_ctx* ctx, int32_t nops,
+                                        const stam_csr_view* ops, const stam_options* opts,
+                                        stam_csr_result* D, stam_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,7 +45,7 @@ class RCsrOut(C.Structure):
 
 class Counters(C.Structure):
     _fields_ = [("mults", C.c_int64), ("adds", C.c_int64), ("ws_inserts", C.c_int64),
-                ("ws_resets", C.c_int64), ("appends", C.c_int64)]
+                ("ws_resets", C.c_int64), ("appends", C.c_int64), ("merge_compares", C.c_int64)]
 
 
 _port = None
@@ -65,6 +65,9 @@ def port_lib():
         lib.oracle_mttkrp_dense.argtypes = [C.POINTER(OCsf3), PD, PD, C.c_int64, C.c_int, PD, PD]
         lib.oracle_mttkrp_sparse.argtypes = [C.POINTER(OCsf3), C.POINTER(OCsrIn),
                                              C.POINTER(OCsrIn), C.c_int, C.POINTER(OCsr)]
+        lib.oracle_ttv.argtypes = [C.POINTER(OCsf3), PD, C.POINTER(OCsr)]
+        lib.oracle_rowdot.argtypes = [C.POINTER(OCsrIn), C.POINTER(OCsrIn), PD, PD]
+        lib.oracle_spadd_merge.argtypes = [C.c_int, C.POINTER(OCsrIn), C.POINTER(OCsr)]
         lib.oracle_free.argtypes = [C.POINTER(OCsr)]
         lib.oracle_last_counters.argtypes = [C.POINTER(Counters)]
         _port = lib
@@ -154,6 +157,43 @@ def spadd(ops, nthreads=1):
     res = OCsr()
     if port_lib().oracle_spadd(len(ops), arr, nthreads, C.byref(res)) != 0:
         raise RuntimeError("oracle_spadd failed")
+    out = _take(res, True)
+    port_lib().oracle_free(C.byref(res))
+    return out
+
+
+def ttv(B, c):
+    """A(i,j) = sum_k B(i,j,k) c(k) (SPEC Fig. ttv), CSR over B's fibers."""
+    keep = []
+    b = _csf_in(B, keep)
+    cv = np.ascontiguousarray(_np(c), dtype=np.float64)
+    res = OCsr()
+    if port_lib().oracle_ttv(C.byref(b), cv.ctypes.data_as(PD), C.byref(res)) != 0:
+        raise RuntimeError("oracle_ttv failed")
+    out = _take(res, True)
+    port_lib().oracle_free(C.byref(res))
+    return out
+
+
+def rowdot(Bm, Cm):
+    """a(i) = sum_j B(i,j) C(i,j) by two-pointer intersection."""
+    keep = []
+    b, c = _csr_in(Bm, keep), _csr_in(Cm, keep)
+    a = np.empty(Bm.nrows)
+    aabs = np.empty(Bm.nrows)
+    if port_lib().oracle_rowdot(C.byref(b), C.byref(c), a.ctypes.data_as(PD),
+                                aabs.ctypes.data_as(PD)) != 0:
+        raise RuntimeError("oracle_rowdot failed")
+    return {"vals": a, "abs": aabs}
+
+
+def spadd_merge(ops):
+    """Merge-based SpAdd baseline: ((op0 + op1) + op2) + ... by two-way unions."""
+    keep = []
+    arr = (OCsrIn * len(ops))(*[_csr_in(o, keep) for o in ops])
+    res = OCsr()
+    if port_lib().oracle_spadd_merge(len(ops), arr, C.byref(res)) != 0:
+        raise RuntimeError("oracle_spadd_merge failed")
     out = _take(res, True)
     port_lib().oracle_free(C.byref(res))
     return out

@@ -18,6 +18,7 @@
 #include "stam_oracle.h"
 
 #include <math.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -526,4 +527,144 @@ int oracle_mttkrp_sparse(const oracle_csf3* B, const oracle_csr_in* C, const ora
   if (C->nrows != B->dims[1] || D->nrows != B->dims[2] || C->ncols != D->ncols) return -2;
   mttkrp_sp_ctx c = {B, C, D, C->ncols};
   return run_rows(B->dims[0], C->ncols, nthreads, &c, mttkrp_sparse_row, C->ncols, A);
+}
+
+/* ------------------------------------------------------------------------ */
+/* SPEC kernels outside the workspace plans                   */
+
+int oracle_ttv(const oracle_csf3* B, const double* c, oracle_csr* A) {
+  memset(A, 0, sizeof(*A));
+  memset(&g_counters, 0, sizeof(g_counters));
+  const int64_t I = B->dims[0], F = B->nfibers;
+  A->nrows = I;
+  A->ncols = B->dims[1];
+  A->nnz = F;
+  A->pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(I + 1));
+  A->idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(F > 0 ? F : 1));
+  A->vals = (double*)malloc(sizeof(double) * (size_t)(F > 0 ? F : 1));
+  A->absv = (double*)malloc(sizeof(double) * (size_t)(F > 0 ? F : 1));
+  if (!A->pos || !A->idx || !A->vals || !A->absv) {
+    oracle_free(A);
+    return -1;
+  }
+  memcpy(A->pos, B->pos1, sizeof(int64_t) * (size_t)(I + 1));
+  for (int64_t f = 0; f < F; f++) {
+    double w = 0.0, wa = 0.0;
+    for (int64_t p = B->pos2[f]; p < B->pos2[f + 1]; p++) {
+      const double t = B->vals[p] * c[B->idx2[p]];
+      w += t;
+      wa += fabs(t);
+      g_counters.mults++;
+      g_counters.adds++;
+    }
+    A->idx[f] = B->idx1[f];
+    A->vals[f] = w;
+    A->absv[f] = wa;
+  }
+  g_counters.appends = F;
+  return 0;
+}
+
+int oracle_rowdot(const oracle_csr_in* B, const oracle_csr_in* C, double* a, double* aabs) {
+  if (B->nrows != C->nrows || B->ncols != C->ncols) return -2;
+  memset(&g_counters, 0, sizeof(g_counters));
+  for (int64_t i = 0; i < B->nrows; i++) {
+    int64_t p = B->pos[i], q = C->pos[i];
+    const int64_t pe = B->pos[i + 1], qe = C->pos[i + 1];
+    double w = 0.0, wa = 0.0;
+    while (p < pe && q < qe) {
+      g_counters.merge_compares++;
+      const int64_t x = B->idx[p], y = C->idx[q];
+      if (x == y) {
+        const double t = B->vals[p] * C->vals[q];
+        w += t;
+        wa += fabs(t);
+        g_counters.mults++;
+        g_counters.adds++;
+        p++;
+        q++;
+      } else if (x < y) {
+        p++;
+      } else {
+        q++;
+      }
+    }
+    a[i] = w;
+    if (aabs) aabs[i] = wa;
+  }
+  return 0;
+}
+
+/* one union co-iteration D = X + Y (row by row): the loop runs while either
+ * row has entries left and compares the two current coordinates (an
+ * exhausted row compares as +inf), one merge_compare per iteration = per
+ * union coordinate (so merge_compares >= nnz(X u Y) - 1). */
+static int union2(const oracle_csr_in* X, const oracle_csr_in* Y, const double* xabs,
+                  const double* yabs, oracle_csr* D) {
+  const int64_t n = X->nrows;
+  memset(D, 0, sizeof(*D));
+  D->nrows = n;
+  D->ncols = X->ncols;
+  const int64_t cap = X->nnz + Y->nnz;
+  D->pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  D->idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(cap > 0 ? cap : 1));
+  D->vals = (double*)malloc(sizeof(double) * (size_t)(cap > 0 ? cap : 1));
+  D->absv = (double*)malloc(sizeof(double) * (size_t)(cap > 0 ? cap : 1));
+  if (!D->pos || !D->idx || !D->vals || !D->absv) {
+    oracle_free(D);
+    return -1;
+  }
+  int64_t o = 0;
+  D->pos[0] = 0;
+  for (int64_t i = 0; i < n; i++) {
+    int64_t p = X->pos[i], q = Y->pos[i];
+    const int64_t pe = X->pos[i + 1], qe = Y->pos[i + 1];
+    while (p < pe || q < qe) {
+      g_counters.merge_compares++;
+      const int64_t x = p < pe ? X->idx[p] : INT64_MAX;
+      const int64_t y = q < qe ? Y->idx[q] : INT64_MAX;
+      if (x == y) {
+        D->idx[o] = x;
+        D->vals[o] = X->vals[p] + Y->vals[q];
+        D->absv[o] = (xabs ? xabs[p] : fabs(X->vals[p])) + (yabs ? yabs[q] : fabs(Y->vals[q]));
+        g_counters.adds++;
+        p++;
+        q++;
+      } else if (x < y) {
+        D->idx[o] = x;
+        D->vals[o] = X->vals[p];
+        D->absv[o] = xabs ? xabs[p] : fabs(X->vals[p]);
+        p++;
+      } else {
+        D->idx[o] = y;
+        D->vals[o] = Y->vals[q];
+        D->absv[o] = yabs ? yabs[q] : fabs(Y->vals[q]);
+        q++;
+      }
+      o++;
+    }
+    D->pos[i + 1] = o;
+  }
+  D->nnz = o;
+  g_counters.appends += o;
+  return 0;
+}
+
+int oracle_spadd_merge(int nops, const oracle_csr_in* ops, oracle_csr* D) {
+  if (nops < 2) return -2;
+  for (int o = 1; o < nops; o++)
+    if (ops[o].nrows != ops[0].nrows || ops[o].ncols != ops[0].ncols) return -2;
+  memset(&g_counters, 0, sizeof(g_counters));
+  oracle_csr acc;
+  int err = union2(&ops[0], &ops[1], NULL, NULL, &acc);
+  for (int o = 2; o < nops && !err; o++) {
+    oracle_csr_in x = {acc.nrows, acc.ncols, acc.nnz, acc.pos, acc.idx, acc.vals};
+    oracle_csr next;
+    err = union2(&x, &ops[o], acc.absv, NULL, &next);
+    oracle_free(&acc);
+    acc = next;
+  }
+  if (err) return err;
+  *D = acc;
+  return 0;
 }

@@ -80,7 +80,25 @@ void oracle_free(oracle_csr* m);
 /* counters of SPEC.md:414-418 for the last call on this thread */
 typedef struct oracle_counters {
   int64_t mults, adds, ws_inserts, ws_resets, appends;
+  int64_t merge_compares; /* co-iteration loop iterations */
 } oracle_counters;
+
+/* TTV (SPEC Fig. ttv; forall(i,j,k) A(i,j) += B(i,j,k)*c(k)): A has B's
+ * (i,j) fibers as its CSR pattern; A(i,j) = ((0 + b1*c(k1)) + b2*c(k2)) + ...
+ * in k order. */
+int oracle_ttv(const oracle_csf3* B, const double* c, oracle_csr* A);
+
+/* row-dot (a(i) = sum(j) B(i,j)*C(i,j), both CSR, no
+ * workspace): two-pointer intersection of the sorted rows, products summed
+ * in j order from 0; one merge_compare per loop iteration. */
+int oracle_rowdot(const oracle_csr_in* B, const oracle_csr_in* C, double* a, double* aabs);
+
+/* Merge-based SpAdd baseline (the paper's comparison to the
+ * workspace plan): D = ((ops[0] + ops[1]) + ops[2]) + ...; each step is a
+ * union co-iteration of two sorted rows while either has entries left
+ * (coinciding entries add, lone entries are copied); one merge_compare per
+ * loop iteration, i.e. per union coordinate. */
+int oracle_spadd_merge(int nops, const oracle_csr_in* ops, oracle_csr* D);
 void oracle_last_counters(oracle_counters* out);
 
 #ifdef __cplusplus

@@ -31,7 +31,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--expt-relaxed-constexpr",
               "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", str(INCLUDE), "-I", str(CSRC)]
 
-CUDA_SOURCES = ["runtime.cpp", "index.cu", "spadd.cu", "spgemm.cu", "mttkrp.cu"]
+CUDA_SOURCES = ["runtime.cpp", "index.cu", "spadd.cu", "spgemm.cu", "mttkrp.cu", "coiter.cu"]
 CXX_SOURCES = ["host/error.cpp", "host/format.cpp", "host/storage.cpp", "host/workspace.cpp",
                "host/kernels.cpp", "host/io.cpp"]
 

@@ -108,6 +108,13 @@ SIGNATURES = {
     "stam_cuda_mttkrp_sparse": (C.c_int, [C.c_void_p, C.POINTER(Csf3View), C.POINTER(CsrView),
                                           C.POINTER(CsrView), C.POINTER(Options),
                                           C.POINTER(CsrResult), C.POINTER(Stats)]),
+    "stam_cuda_ttv": (C.c_int, [C.c_void_p, C.POINTER(Csf3View), C.POINTER(DenseView),
+                                C.POINTER(Options), C.POINTER(CsrResult), C.POINTER(Stats)]),
+    "stam_cuda_rowdot": (C.c_int, [C.c_void_p, C.POINTER(CsrView), C.POINTER(CsrView),
+                                   C.POINTER(Options), C.POINTER(DenseResult), C.POINTER(Stats)]),
+    "stam_cuda_spadd_merge": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(CsrView),
+                                        C.POINTER(Options), C.POINTER(CsrResult),
+                                        C.POINTER(Stats)]),
 }
 
 _lock = threading.Lock()

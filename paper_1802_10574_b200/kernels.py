@@ -181,6 +181,39 @@ class Context:
                                                   C.byref(r), C.byref(st)))
         return self._csr_out(r)
 
+    # -- SPEC kernels outside the workspace plans ------------------------------
+    def ttv(self, B: CSF3, c, *, result: str = "device", timing: bool = False,
+            stats: Optional[N.Stats] = None) -> CSR:
+        """A(i,j) = sum_k B(i,j,k) c(k): CSR over B's (i,j) fibers."""
+        cv = c if isinstance(c, Dense) else Dense(c.reshape(-1, 1) if hasattr(c, "reshape") else c)
+        r = N.CsrResult()
+        st = stats if stats is not None else N.Stats()
+        opts = self.options(True, result, timing)
+        N.check(self._lib.stam_cuda_ttv(self._ctx, C.byref(B.view()), C.byref(cv.view()),
+                                        C.byref(opts), C.byref(r), C.byref(st)))
+        return self._csr_out(r)
+
+    def rowdot(self, B: CSR, Cm: CSR, *, result: str = "device", timing: bool = False,
+               stats: Optional[N.Stats] = None) -> Dense:
+        """a(i) = sum_j B(i,j) C(i,j) (two-way intersection, no workspace)."""
+        r = N.DenseResult()
+        st = stats if stats is not None else N.Stats()
+        opts = self.options(True, result, timing)
+        N.check(self._lib.stam_cuda_rowdot(self._ctx, C.byref(B.view()), C.byref(Cm.view()),
+                                           C.byref(opts), C.byref(r), C.byref(st)))
+        return self._dense_out(r)
+
+    def spadd_merge(self, ops: Sequence[CSR], *, result: str = "device", timing: bool = False,
+                    stats: Optional[N.Stats] = None) -> CSR:
+        """Merge-based SpAdd baseline: pairwise two-way unions."""
+        views = (N.CsrView * len(ops))(*[o.view() for o in ops])
+        r = N.CsrResult()
+        st = stats if stats is not None else N.Stats()
+        opts = self.options(True, result, timing)
+        N.check(self._lib.stam_cuda_spadd_merge(self._ctx, len(ops), views, C.byref(opts),
+                                                C.byref(r), C.byref(st)))
+        return self._csr_out(r)
+
     def mttkrp(self, B: CSF3, Cf, Df, *, result: str = "device", timing: bool = False,
                stats: Optional[N.Stats] = None):
         """Dense factors (``Dense``) give a dense A; CSR factors give a CSR A."""
