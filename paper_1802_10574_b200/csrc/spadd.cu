@@ -34,10 +34,26 @@ namespace stamgpu {
 namespace {
 
 constexpr int kMaxOps = 16;
-constexpr int kWarps = 8;
-constexpr int kRowsPerWarp = 2;
-constexpr int kTileRows = kWarps * kRowsPerWarp;
-constexpr int kStage = 384;  // staged entries per warp
+
+// Tile shapes: warps per CTA, rows per warp, staged entries per warp.  Short
+// rows (the common case) use many rows per tile; rows averaging a few hundred
+// entries use one row per warp and a deeper staging buffer.
+template <int W, int RPW, int STAGE>
+struct TileCfg {
+  static constexpr int kWarps = W;
+  static constexpr int kRowsPerWarp = RPW;
+  static constexpr int kTileRows = W * RPW;
+  static constexpr int kStage = STAGE;
+};
+#ifndef SPADD_MID_WARPS
+#define SPADD_MID_WARPS 4
+#endif
+#ifndef SPADD_MID_STAGE
+#define SPADD_MID_STAGE 768
+#endif
+using ShortRows = TileCfg<8, 2, 384>;
+using MidRowsCfg = TileCfg<SPADD_MID_WARPS, 1, SPADD_MID_STAGE>;
+constexpr int kStageMin = 384;
 
 enum RowState : int { kStaged = 0, kPostponed = 1, kDeferred = 2 };
 
@@ -62,26 +78,27 @@ struct SpaddParams {
   int64_t* total_nnz;
 };
 
-template <typename ColT>
+template <typename ColT, int STAGE>
 struct WarpStage {
-  ColT in_col[kStage];
-  ColT st_col[kStage];
-  double st_val[kStage];
-  uint8_t st_op[kStage];
+  static constexpr int kStage = STAGE;
+  ColT in_col[STAGE];
+  ColT st_col[STAGE];
+  double st_val[STAGE];
+  uint8_t st_op[STAGE];
   // current row's operand segments
   int64_t seg_beg[kMaxOps];
   int seg_len[kMaxOps];
   int seg_co[kMaxOps];
 };
 
-template <typename ColT>
+template <typename ColT, typename Cfg>
 struct TileSmem {
-  WarpStage<ColT> w[kWarps];
-  int64_t tpos[kMaxOps][kTileRows + 1];
-  int64_t row_cnt[kTileRows];
-  int64_t row_dst[kTileRows];
-  int row_state[kTileRows];
-  int row_off[kTileRows];
+  WarpStage<ColT, Cfg::kStage> w[Cfg::kWarps];
+  int64_t tpos[kMaxOps][Cfg::kTileRows + 1];
+  int64_t row_cnt[Cfg::kTileRows];
+  int64_t row_dst[Cfg::kTileRows];
+  int row_state[Cfg::kTileRows];
+  int row_off[Cfg::kTileRows];
   int64_t tile_id;
 };
 
@@ -122,9 +139,8 @@ __device__ __forceinline__ int64_t lower_bound_global(const int64_t* s, int64_t 
 }
 
 // Fill the warp's segment table for tile row r; returns the exact total.
-template <typename ColT>
-__device__ __forceinline__ int64_t row_segments(const TileSmem<ColT>& S, WarpStage<ColT>& W,
-                                                int nops, int r) {
+template <typename SM, typename WS>
+__device__ __forceinline__ int64_t row_segments(const SM& S, WS& W, int nops, int r) {
   const unsigned lane = lane_id();
   int64_t b = 0, e = 0;
   if ((int)lane < nops) {
@@ -145,8 +161,8 @@ __device__ __forceinline__ int64_t row_segments(const TileSmem<ColT>& S, WarpSta
 }
 
 // Stage the row's column segments, concatenated in operand order, into in_col.
-template <typename ColT>
-__device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT>& W) {
+template <typename ColT, int STAGE>
+__device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT, STAGE>& W) {
   const unsigned lane = lane_id();
   for (int p = 0; p < P.nops; p++) {
     const int64_t* src = P.idx[p] + W.seg_beg[p];
@@ -159,8 +175,8 @@ __device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT>&
 
 // Rank-merge the staged row into st_* at [out, out+L) (operand order on ties),
 // then combine equal columns in place.  Returns the number of distinct columns.
-template <typename ColT>
-__device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int out) {
+template <typename ColT, int STAGE>
+__device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L, int out) {
   const unsigned lane = lane_id();
   const int nops = P.nops;
   ColT* st_col = W.st_col + out;
@@ -229,8 +245,8 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT>& W, int L, int ou
 }
 
 // Distinct-column count of a staged row (in_col only, no merge written).
-template <typename ColT>
-__device__ int count_row(const SpaddParams& P, const WarpStage<ColT>& W) {
+template <typename ColT, int STAGE>
+__device__ int count_row(const SpaddParams& P, const WarpStage<ColT, STAGE>& W) {
   const unsigned lane = lane_id();
   int count = W.seg_len[0];  // every first-operand entry starts a column
   for (int o = 1; o < P.nops; o++) {
@@ -257,8 +273,8 @@ __device__ int count_row(const SpaddParams& P, const WarpStage<ColT>& W) {
 
 // Distinct-column count of a row read straight from global memory (rows that
 // exceed the staging buffer; their values are written by the long-row kernel).
-template <typename ColT>
-__device__ int64_t count_row_global(const SpaddParams& P, const TileSmem<ColT>& S, int r) {
+template <typename SM>
+__device__ int64_t count_row_global(const SpaddParams& P, const SM& S, int r) {
   const unsigned lane = lane_id();
   int64_t count = S.tpos[0][r + 1] - S.tpos[0][r];
   for (int o = 1; o < P.nops; o++) {
@@ -281,10 +297,14 @@ __device__ int64_t count_row_global(const SpaddParams& P, const TileSmem<ColT>& 
   return count;
 }
 
-template <typename ColT>
-__global__ void __launch_bounds__(kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
+template <typename ColT, typename Cfg>
+__global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
+  constexpr int kWarps = Cfg::kWarps;
+  constexpr int kRowsPerWarp = Cfg::kRowsPerWarp;
+  constexpr int kTileRowsC = Cfg::kTileRows;
+  constexpr int kStage = Cfg::kStage;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem<ColT>& S = *reinterpret_cast<TileSmem<ColT>*>(smem_raw);
+  TileSmem<ColT, Cfg>& S = *reinterpret_cast<TileSmem<ColT, Cfg>*>(smem_raw);
   const unsigned lane = lane_id();
   const int warp = threadIdx.x >> 5;
   const int nops = P.nops;
@@ -292,18 +312,18 @@ __global__ void __launch_bounds__(kWarps * 32) spadd_tiles_kernel(const SpaddPar
   if (threadIdx.x == 0) S.tile_id = P.tile_base + (int64_t)atomicAdd(P.tile_counter, 1ull);
   __syncthreads();
   const int64_t tile = S.tile_id;
-  const int64_t row0 = tile * kTileRows;
-  const int nrows_tile = (int)min((int64_t)kTileRows, P.nrows - row0);
+  const int64_t row0 = tile * kTileRowsC;
+  const int nrows_tile = (int)min((int64_t)kTileRowsC, P.nrows - row0);
 
   // tile-wide operand row pointers
-  for (int i = threadIdx.x; i < nops * (kTileRows + 1); i += blockDim.x) {
-    const int p = i / (kTileRows + 1);
-    const int r = i % (kTileRows + 1);
+  for (int i = threadIdx.x; i < nops * (kTileRowsC + 1); i += blockDim.x) {
+    const int p = i / (kTileRowsC + 1);
+    const int r = i % (kTileRowsC + 1);
     S.tpos[p][r] = (r <= nrows_tile) ? __ldg(P.pos[p] + row0 + r) : 0;
   }
   __syncthreads();
 
-  WarpStage<ColT>& W = S.w[warp];
+  WarpStage<ColT, kStage>& W = S.w[warp];
   int stage_off = 0;
   for (int k = 0; k < kRowsPerWarp; k++) {
     const int r = warp * kRowsPerWarp + k;
@@ -392,6 +412,132 @@ __global__ void __launch_bounds__(kWarps * 32) spadd_tiles_kernel(const SpaddPar
 // prefix, zeroes the window's output slots and then applies the operands in
 // order (assign, then accumulate) — the workspace semantics, bit-exact.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Mid rows (a warp's staging < row <= kMid elements): one CTA per row, the
+// same rank-scatter as merge_row over the whole CTA (elements ranked by
+// binary search in the other operands' staged segments), then equal columns
+// combined in operand order and compacted by a block scan.
+constexpr int kMid = 3072;
+constexpr int kMidThreads = 256;
+
+struct MidSmem {
+  int64_t in_col[kMid];
+  double in_val[kMid];
+  int64_t st_col[kMid];
+  double st_val[kMid];
+  uint8_t st_op[kMid];
+  int64_t seg_beg[kMaxOps];
+  int seg_len[kMaxOps];
+  int seg_co[kMaxOps + 1];
+  int scan[33];
+  int dup;
+};
+
+__device__ __forceinline__ int rank_g(const int64_t* s, int n, int64_t x, bool upper) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    const bool before = upper ? s[lo + h] <= x : s[lo + h] < x;
+    if (before) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kMidThreads) spadd_mid_rows_kernel(const SpaddParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MidSmem& S = *reinterpret_cast<MidSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int nops = P.nops;
+  const unsigned long long ndef = *P.deferred_count;
+  for (unsigned long long d = blockIdx.x; d < ndef; d += gridDim.x) {
+    const int64_t r = P.deferred_rows[d];
+    if (tid < nops) {
+      S.seg_beg[tid] = __ldg(P.pos[tid] + r);
+      S.seg_len[tid] = (int)min((int64_t)kMid + 1, __ldg(P.pos[tid] + r + 1) - S.seg_beg[tid]);
+    }
+    if (tid == 0) S.dup = 0;
+    __syncthreads();
+    if (tid == 0) {
+      int co = 0;
+      for (int p = 0; p < nops; p++) {
+        S.seg_co[p] = co;
+        co = min(co + S.seg_len[p], kMid + 1);
+      }
+      S.seg_co[nops] = co;
+    }
+    __syncthreads();
+    const int L = S.seg_co[nops];
+    if (L > kMid) {  // spadd_long_rows_kernel's row
+      __syncthreads();
+      continue;
+    }
+    const int64_t dst = P.out_pos[r];
+    for (int p = 0; p < nops; p++) {
+      const int64_t b = S.seg_beg[p];
+      const int co = S.seg_co[p];
+      for (int t = tid; t < S.seg_len[p]; t += kMidThreads) {
+        S.in_col[co + t] = __ldg(P.idx[p] + b + t);
+        S.in_val[co + t] = P.values ? __ldg(P.vals[p] + b + t) : 0.0;
+      }
+    }
+    __syncthreads();
+    bool dup = false;
+    for (int e = tid; e < L; e += kMidThreads) {
+      int o = 0;
+      while (o + 1 < nops && S.seg_co[o + 1] <= e) o++;
+      const int64_t x = S.in_col[e];
+      int m = e - S.seg_co[o];
+      for (int q = 0; q < nops; q++) {
+        if (q == o) continue;
+        const int64_t* sq = S.in_col + S.seg_co[q];
+        const int rq = rank_g(sq, S.seg_len[q], x, q < o);
+        if (q < o && rq > 0 && sq[rq - 1] == x) dup = true;
+        m += rq;
+      }
+      S.st_col[m] = x;
+      S.st_val[m] = S.in_val[e];
+      S.st_op[m] = (uint8_t)o;
+    }
+    if (dup) S.dup = 1;
+    __syncthreads();
+    if (!S.dup) {
+      for (int m = tid; m < L; m += kMidThreads) {
+        P.out_idx[dst + m] = S.st_col[m];
+        P.out_vals[dst + m] = S.st_val[m];
+      }
+    } else {
+      int run = 0;
+      for (int base = 0; base < L; base += kMidThreads) {
+        const int m = base + tid;
+        bool lead = false;
+        double w = 0.0;
+        int64_t x = 0;
+        if (m < L) {
+          x = S.st_col[m];
+          lead = m == 0 || S.st_col[m - 1] != x;
+          if (lead) {
+            w = S.st_op[m] == 0 ? S.st_val[m] : add_rn(0.0, S.st_val[m]);
+            for (int n = m + 1; n < L && S.st_col[n] == x; n++) w = add_rn(w, S.st_val[n]);
+          }
+        }
+        int tot;
+        const int ex = block_exclusive_scan(lead ? 1 : 0, S.scan, &tot);
+        if (lead) {
+          P.out_idx[dst + run + ex] = x;
+          P.out_vals[dst + run + ex] = w;
+        }
+        run += tot;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 constexpr int kLongThreads = 512;
 constexpr int kWinWords = 2048;
 constexpr int64_t kWinBits = (int64_t)kWinWords * 32;
@@ -414,6 +560,12 @@ __global__ void __launch_bounds__(kLongThreads) spadd_long_rows_kernel(const Spa
     for (int w = tid; w < kWinWords; w += blockDim.x) bits[w] = 0u;
     int64_t dst = P.out_pos[r];
     __syncthreads();
+    int64_t row_len = 0;
+    for (int p = 0; p < nops; p++) row_len += stop[p] - head[p];
+    if (row_len <= kMid) {  // spadd_mid_rows_kernel's row
+      __syncthreads();
+      continue;
+    }
     while (true) {
       if (tid == 0) {
         int64_t c0 = INT64_MAX;
@@ -472,14 +624,14 @@ __global__ void __launch_bounds__(kLongThreads) spadd_long_rows_kernel(const Spa
   }
 }
 
-template <typename ColT>
+template <typename ColT, typename Cfg>
 void launch_tiles(stamrt::Call& call, const SpaddParams& P, int64_t ntiles) {
   if (ntiles <= 0) return;
-  const size_t smem = sizeof(TileSmem<ColT>);
-  auto kern = spadd_tiles_kernel<ColT>;
+  const size_t smem = sizeof(TileSmem<ColT, Cfg>);
+  auto kern = spadd_tiles_kernel<ColT, Cfg>;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   call.before_launch(sizeof(ColT) == 4 ? "spadd_tiles<u32>" : "spadd_tiles<i64>");
-  kern<<<(unsigned)ntiles, kWarps * 32, smem, call.stream()>>>(P);
+  kern<<<(unsigned)ntiles, Cfg::kWarps * 32, smem, call.stream()>>>(P);
   call.after_launch();
 }
 
@@ -537,7 +689,6 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     SpaddParams P{};
     P.nops = nops;
     P.nrows = nrows;
-    P.ntiles = ceil_div(nrows, kTileRows);
     P.values = call.opts().mode == STAM_MODE_FUSED;
     int64_t cap = 0, accum = 0, in_bytes = 0;
     bool host_in = false;
@@ -547,6 +698,10 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
       host_in |= ops[p].mem == STAM_MEM_HOST;
       in_bytes += ops[p].nnz * 16;
     }
+    // rows averaging a few hundred entries: one row per warp, deeper staging
+    const bool mid_rows = ncols <= (int64_t)UINT32_MAX && nrows > 0 && cap / nrows > 360;
+    const int64_t kTileRows = mid_rows ? MidRowsCfg::kTileRows : ShortRows::kTileRows;
+    P.ntiles = ceil_div(nrows, kTileRows);
     const bool host_out = call.opts().result_mem == STAM_MEM_HOST;
     // Host operands or a host result: stream row blocks.  Block k's operand
     // ranges go up on the copy stream while earlier blocks merge, and each
@@ -588,7 +743,7 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     P.deferred_count = reinterpret_cast<unsigned long long*>(ctl);
     P.total_nnz = reinterpret_cast<int64_t*>(ctl + 1);
     P.tile_status = ctl + 4 + nblocks;
-    const int64_t max_deferred = std::min<int64_t>(nrows, cap / kStage + 1);
+    const int64_t max_deferred = std::min<int64_t>(nrows, cap / kStageMin + 1);
     P.deferred_rows = call.scratch_n<int64_t>((size_t)max_deferred);
     int64_t* marks = host_out ? call.marks() : nullptr;
 
@@ -613,10 +768,14 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
       P.last_tile = t1 - 1;
       P.block_end = marks ? marks + k : nullptr;
       P.tile_counter = reinterpret_cast<unsigned long long*>(ctl + 4 + k);
-      if (ncols <= (int64_t)UINT32_MAX)
-        launch_tiles<uint32_t>(call, P, t1 - t0);
-      else
-        launch_tiles<int64_t>(call, P, t1 - t0);
+      if (ncols <= (int64_t)UINT32_MAX) {
+        if (mid_rows)
+          launch_tiles<uint32_t, MidRowsCfg>(call, P, t1 - t0);
+        else
+          launch_tiles<uint32_t, ShortRows>(call, P, t1 - t0);
+      } else {
+        launch_tiles<int64_t, ShortRows>(call, P, t1 - t0);
+      }
       if (host_out) {
         done[(size_t)k] = call.event();
         STAM_CUDA_CHECK(cudaEventRecord(done[(size_t)k], call.stream()));
@@ -643,7 +802,17 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
         if (issued < nblocks) issue_block(issued++);
       }
     }
-    // rows too long for a warp's staging (deferred by their tiles)
+    // rows too long for a warp's staging (deferred by their tiles): mid rows
+    // by a CTA each, the longest by the windowed bitmap kernel
+    {
+      const size_t msmem = sizeof(MidSmem);
+      STAM_CUDA_CHECK(cudaFuncSetAttribute(spadd_mid_rows_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+      call.before_launch("spadd_mid_rows");
+      spadd_mid_rows_kernel<<<(unsigned)std::max(1, call.ctx()->num_sms * 2), kMidThreads, msmem,
+                              call.stream()>>>(P);
+      call.after_launch();
+    }
     call.before_launch("spadd_long_rows");
     spadd_long_rows_kernel<<<(unsigned)std::max(1, call.ctx()->num_sms), kLongThreads, 0,
                              call.stream()>>>(P);

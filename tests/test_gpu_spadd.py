@@ -117,3 +117,21 @@ def test_spadd_arity(ctx):
     with pytest.raises(StamError) as e:
         ctx.spadd(_dev([a]))
     assert e.value.code == "ArityMismatch"
+
+
+def test_spadd_mid_rows_take_the_cta_path(ctx):
+    # rows between a warp's staging (384) and the CTA path's 3072 entries, some
+    # with many shared columns, plus rows on either side of both limits
+    rng = np.random.default_rng(17)
+    ops = []
+    for k in range(4):
+        lens = rng.integers(100, 900, size=300)
+        lens[[0, 1, 2, 3]] = [96, 97, 800, 1000]
+        pos = np.zeros(301, dtype=np.int64)
+        np.cumsum(lens, out=pos[1:])
+        ops.append(G.csr_from_lengths(300, 3000, pos, 500 + k))
+    D = ctx.spadd(_dev(ops))
+    oracle.compare_csr(D, oracle.spadd(ops), exact_values=True)
+    # assemble mode through the same path
+    Dz = ctx.spadd(_dev(ops), mode="assemble")
+    assert np.array_equal(Dz.idx.cpu().numpy(), D.idx.cpu().numpy())
