@@ -63,4 +63,18 @@ TensorStorage spaddCompute(std::span<const TensorStorage* const> ops,
 TensorStorage mttkrp(const TensorStorage& B, const TensorStorage& C, const TensorStorage& D,
                      const KernelOptions& = {}, ExecutionStats* = nullptr);
 
+/// TTV (SPEC Fig. ttv): A(i,j) = sum_k B(i,j,k) c(k); B csf(3), c a dense
+/// vector (denseFormat(1) or (2)) of dims[2] values; A csr() over B's fibers.
+TensorStorage ttv(const TensorStorage& B, const TensorStorage& c, const KernelOptions& = {},
+                  ExecutionStats* = nullptr);
+
+/// row-dot: a(i) = sum_j B(i,j) C(i,j) by intersection; csr()
+/// inputs, denseFormat(1) result; stats->merge_compares = loop iterations.
+TensorStorage rowdot(const TensorStorage& B, const TensorStorage& C, const KernelOptions& = {},
+                     ExecutionStats* = nullptr);
+
+/// Merge-based SpAdd baseline: pairwise two-way unions.
+TensorStorage spaddMerge(std::span<const TensorStorage* const> ops, const KernelOptions& = {},
+                         ExecutionStats* = nullptr);
+
 }  // namespace stam

@@ -33,7 +33,7 @@ NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--expt-relaxed-constexpr",
 
 CUDA_SOURCES = ["runtime.cpp", "index.cu", "spadd.cu", "spgemm.cu", "mttkrp.cu", "coiter.cu"]
 CXX_SOURCES = ["host/error.cpp", "host/format.cpp", "host/storage.cpp", "host/workspace.cpp",
-               "host/kernels.cpp", "host/io.cpp"]
+               "host/kernels.cpp", "host/io.cpp", "host/execute.cpp"]
 
 
 def _nvcc() -> str:

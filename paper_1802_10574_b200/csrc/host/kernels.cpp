@@ -228,4 +228,75 @@ TensorStorage mttkrp(const TensorStorage& B, const TensorStorage& C, const Tenso
   return adoptCsr(ctx, r);
 }
 
+namespace {
+stam_csf3_view csfView(const TensorStorage& B) {
+  stam_csf3_view b{};
+  for (int d = 0; d < 3; d++) b.dims[d] = B.dimensions()[(size_t)d];
+  b.nfibers = (int64_t)B.level(1).idx.size();
+  b.nnz = B.storedCount();
+  b.pos1 = B.level(1).pos.data();
+  b.idx1 = B.level(1).idx.data();
+  b.pos2 = B.level(2).pos.data();
+  b.idx2 = B.level(2).idx.data();
+  b.vals = B.vals().data();
+  b.mem = STAM_MEM_HOST;
+  return b;
+}
+}  // namespace
+
+TensorStorage ttv(const TensorStorage& B, const TensorStorage& c, const KernelOptions& o,
+                  ExecutionStats* stats) {
+  require(B, csf(3), "ttv B");
+  if (!c.format().allDense()) fail(ErrorCode::PreconditionViolated, "ttv: c must be dense");
+  if (c.storedCount() != B.dimensions()[2])
+    fail(ErrorCode::DimensionMismatch, "ttv: c must hold dims[2] values");
+  const stam_csf3_view b = csfView(B);
+  const stam_dense_view cv{c.storedCount(), 1, c.vals().data(), STAM_MEM_HOST, 0};
+  stam_cuda_ctx* ctx = context(o.device);
+  const stam_options opts = options(o);
+  stam_csr_result r{};
+  stam_stats st{};
+  check(stam_cuda_ttv(ctx, &b, &cv, &opts, &r, &st));
+  report(st, stats);
+  return adoptCsr(ctx, r);
+}
+
+TensorStorage rowdot(const TensorStorage& B, const TensorStorage& C, const KernelOptions& o,
+                     ExecutionStats* stats) {
+  require(B, csr(), "rowdot B");
+  require(C, csr(), "rowdot C");
+  if (B.dimensions() != C.dimensions())
+    fail(ErrorCode::DimensionMismatch, "rowdot: B and C must have equal dimensions");
+  const stam_csr_view b = csrView(B), c = csrView(C);
+  stam_cuda_ctx* ctx = context(o.device);
+  const stam_options opts = options(o);
+  stam_dense_result r{};
+  stam_stats st{};
+  check(stam_cuda_rowdot(ctx, &b, &c, &opts, &r, &st));
+  report(st, stats);
+  TensorStorage out({r.nrows}, denseFormat(1));
+  std::memcpy(out.vals().data(), r.vals, sizeof(double) * (size_t)r.nrows);
+  check(stam_cuda_release(ctx, r.handle));
+  return out;
+}
+
+TensorStorage spaddMerge(std::span<const TensorStorage* const> ops, const KernelOptions& o,
+                         ExecutionStats* stats) {
+  if (ops.size() < 2) fail(ErrorCode::ArityMismatch, "spadd needs at least two operands");
+  std::vector<stam_csr_view> views;
+  for (const TensorStorage* t : ops) {
+    require(*t, csr(), "spadd operand");
+    if (t->dimensions() != ops[0]->dimensions())
+      fail(ErrorCode::DimensionMismatch, "spadd operands must have equal dimensions");
+    views.push_back(csrView(*t));
+  }
+  stam_cuda_ctx* ctx = context(o.device);
+  const stam_options opts = options(o);
+  stam_csr_result r{};
+  stam_stats st{};
+  check(stam_cuda_spadd_merge(ctx, (int32_t)views.size(), views.data(), &opts, &r, &st));
+  report(st, stats);
+  return adoptCsr(ctx, r);
+}
+
 }  // namespace stam

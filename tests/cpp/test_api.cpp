@@ -9,8 +9,10 @@
 
 #include <cstdio>
 #include <fstream>
+#include <map>
 #include <string>
 
+#include "stam/execute.h"
 #include "stam/io.h"
 #include "stam/kernels.h"
 #include "stam/storage.h"
@@ -192,6 +194,81 @@ TEST_CASE("gpu: assemble / compute modes and unsorted output") {
   TensorStorage sidx = spadd(ops, asm_opts);
   TensorStorage S = spaddCompute(ops, sidx);
   CHECK(S.vals() == std::vector<double>{5, 2, 5, 9});
+}
+
+TEST_CASE("execute: CIN parse errors and unsupported plans (host)") {
+  std::map<std::string, const TensorStorage*> none;
+  CHECK_THROWS_AS(execute("forall(i) (A(i) = ", none), Error);
+  try {
+    execute("forall(i,j) A(i,j) = B(i,j) + C(i,j) + D(i,j)", none);
+    FAIL("expected UnsupportedMerge");
+  } catch (const Error& e) {
+    CHECK(e.code() == ErrorCode::UnsupportedMerge);
+  }
+  try {
+    execute("forall(i,k,j) A(i,j) += B(i,k)*C(k,j)", none);
+    FAIL("expected UnplannableResult");
+  } catch (const Error& e) {
+    CHECK(e.code() == ErrorCode::UnplannableResult);
+  }
+  try {
+    execute("forall(i) ((forall(j) A(i,j) = w0(j)) where (forall(k,j) w0(j) += B(i,k)*C(k,j)))",
+            none);
+    FAIL("expected MissingBinding");
+  } catch (const Error& e) {
+    CHECK(e.code() == ErrorCode::MissingBinding);
+  }
+}
+
+TEST_CASE("gpu: execute dispatches the golden CIN plans") {
+  if (!g_gpu) return;
+  TensorStorage B = csrOf(2, 2, {0, 2, 3}, {0, 1, 1}, {1, 2, 3});
+  TensorStorage C = csrOf(2, 2, {0, 1, 3}, {0, 0, 1}, {4, 5, 6});
+  TensorStorage D = csrOf(2, 2, {0, 1, 1}, {1}, {10});
+  // test_transform.cpp:141-147 printed form
+  ExecuteResult g = execute(
+      "forall(i) ((forall(j) A(i,j) = w0(j)) where (forall(k,j) w0(j) += B(i,k)*C(k,j)))",
+      {{"B", &B}, {"C", &C}});
+  CHECK(g.plan == "spgemm");
+  CHECK(g.tensor == "A");
+  CHECK(g.result.vals() == std::vector<double>{14, 12, 15, 18});
+  // test_transform.cpp:275-284 printed form
+  ExecuteResult a = execute(
+      "forall(i) ((forall(j) A(i,j) = w0(j)) where ((forall(j) w0(j) = B(i,j) ; forall(j) w0(j) "
+      "+= C(i,j) ; forall(j) w0(j) += D(i,j))))",
+      {{"B", &B}, {"C", &C}, {"D", &D}});
+  CHECK(a.plan == "spadd");
+  CHECK(a.result.vals() == std::vector<double>{5, 12, 5, 9});
+  ExecuteResult m = execute("forall(i,j) A(i,j) = B(i,j) + C(i,j)", {{"B", &B}, {"C", &C}});
+  CHECK(m.plan == "spadd_merge");
+  CHECK(m.result.vals() == std::vector<double>{5, 2, 5, 9});
+  ExecuteResult rd = execute("forall(i,j) a(i) += B(i,j)*C(i,j)", {{"B", &B}, {"C", &C}});
+  CHECK(rd.plan == "rowdot");
+  CHECK(rd.result.vals() == std::vector<double>{4, 18});
+  // MTTKRP, golden naming (test_transform.cpp:166-184): B(i,k,l), C(l,j), D(k,j)
+  TensorStorage T = fromCoo({2, 2, 2}, csf(3), {{{0, 0, 0}, 1.0}, {{0, 1, 1}, 2.0}, {{1, 1, 0}, 3.0}});
+  TensorStorage Cd({2, 2}, denseFormat(2)), Dd({2, 2}, denseFormat(2));
+  Cd.vals() = {5, 6, 7, 8};  // C(l,j): indexed by the innermost mode
+  Dd.vals() = {1, 2, 3, 4};  // D(k,j): indexed by the middle mode
+  ExecuteResult md = execute(
+      "forall(i,k) ((forall(j) A(i,j) += w0(j)*D(k,j)) where (forall(l,j) w0(j) += "
+      "B(i,k,l)*C(l,j)))",
+      {{"B", &T}, {"C", &Cd}, {"D", &Dd}});
+  CHECK(md.plan == "mttkrp_dense");
+  CHECK(md.result.vals() == std::vector<double>{47, 76, 45, 72});
+  TensorStorage Cs = csrOf(2, 2, {0, 2, 3}, {0, 1, 1}, {5, 6, 8});
+  TensorStorage Ds = csrOf(2, 2, {0, 1, 3}, {0, 0, 1}, {1, 3, 4});
+  ExecuteResult ms = execute(
+      "forall(i) ((forall(j) A(i,j) = w1(j)) where (forall(k) ((forall(j) w1(j) += w0(j)*D(k,j)) "
+      "where (forall(l,j) w0(j) += B(i,k,l)*C(l,j)))))",
+      {{"B", &T}, {"C", &Cs}, {"D", &Ds}});
+  CHECK(ms.plan == "mttkrp_sparse");
+  CHECK(ms.result.vals() == std::vector<double>{5, 64, 45, 72});
+  TensorStorage c({2}, denseFormat(1));
+  c.vals() = {2, 3};
+  ExecuteResult tv = execute("forall(i,j,k) A(i,j) += B(i,j,k)*c(k)", {{"B", &T}, {"c", &c}});
+  CHECK(tv.plan == "ttv");
+  CHECK(tv.result.vals() == std::vector<double>{2, 6, 6});
 }
 
 static int g_init = [] {
