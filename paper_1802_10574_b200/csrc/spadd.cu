@@ -161,10 +161,13 @@ __device__ __forceinline__ int64_t row_segments(const SM& S, WS& W, int nops, in
 }
 
 // Stage the row's column segments, concatenated in operand order, into in_col.
-template <typename ColT, int STAGE>
+template <int NOPS, typename ColT, int STAGE>
 __device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT, STAGE>& W) {
   const unsigned lane = lane_id();
-  for (int p = 0; p < P.nops; p++) {
+  const int nops = NOPS ? NOPS : P.nops;
+#pragma unroll
+  for (int p = 0; p < (NOPS ? NOPS : kMaxOps); p++) {
+    if (!NOPS && p >= nops) break;
     const int64_t* src = P.idx[p] + W.seg_beg[p];
     const int len = W.seg_len[p];
     ColT* dst = W.in_col + W.seg_co[p];
@@ -175,16 +178,18 @@ __device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT, 
 
 // Rank-merge the staged row into st_* at [out, out+L) (operand order on ties),
 // then combine equal columns in place.  Returns the number of distinct columns.
-template <typename ColT, int STAGE>
+template <int NOPS, typename ColT, int STAGE>
 __device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L, int out) {
   const unsigned lane = lane_id();
-  const int nops = P.nops;
+  const int nops = NOPS ? NOPS : P.nops;
   ColT* st_col = W.st_col + out;
   double* st_val = W.st_val + out;
   uint8_t* st_op = W.st_op + out;
   // scatter every element to its merged slot
   bool dup = false;
-  for (int o = 0; o < nops; o++) {
+#pragma unroll
+  for (int o = 0; o < (NOPS ? NOPS : kMaxOps); o++) {
+    if (!NOPS && o >= nops) break;
     const double* vsrc = P.vals[o] + W.seg_beg[o];
     const int len = W.seg_len[o];
     const int co = W.seg_co[o];
@@ -192,7 +197,9 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
       const double v = P.values ? ldg_stream(vsrc + t) : 0.0;
       const ColT x = W.in_col[co + t];
       int m = t;
-      for (int q = 0; q < nops; q++) {
+#pragma unroll
+      for (int q = 0; q < (NOPS ? NOPS : kMaxOps); q++) {
+        if (!NOPS && q >= nops) break;
         if (q == o) continue;
         const ColT* sq = W.in_col + W.seg_co[q];
         const int nq = W.seg_len[q];
@@ -245,7 +252,7 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
 }
 
 // Distinct-column count of a staged row (in_col only, no merge written).
-template <typename ColT, int STAGE>
+template <int NOPS, typename ColT, int STAGE>
 __device__ int count_row(const SpaddParams& P, const WarpStage<ColT, STAGE>& W) {
   const unsigned lane = lane_id();
   int count = W.seg_len[0];  // every first-operand entry starts a column
@@ -297,7 +304,7 @@ __device__ int64_t count_row_global(const SpaddParams& P, const SM& S, int r) {
   return count;
 }
 
-template <typename ColT, typename Cfg>
+template <typename ColT, typename Cfg, int NOPS>
 __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
   constexpr int kWarps = Cfg::kWarps;
   constexpr int kRowsPerWarp = Cfg::kRowsPerWarp;
@@ -332,12 +339,12 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     int64_t cnt;
     int state;
     if (tot <= kStage - stage_off) {
-      load_cols(P, W);
-      cnt = merge_row(P, W, (int)tot, stage_off);
+      load_cols<NOPS>(P, W);
+      cnt = merge_row<NOPS>(P, W, (int)tot, stage_off);
       state = kStaged;
     } else if (tot <= kStage) {
-      load_cols(P, W);
-      cnt = count_row(P, W);
+      load_cols<NOPS>(P, W);
+      cnt = count_row<NOPS>(P, W);
       state = kPostponed;
     } else {
       cnt = count_row_global(P, S, r);
@@ -392,8 +399,8 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     if (state == kPostponed) {
       const int64_t dst = S.row_dst[r];
       const int64_t tot = row_segments(S, W, nops, r);
-      load_cols(P, W);
-      const int cnt = merge_row(P, W, (int)tot, 0);
+      load_cols<NOPS>(P, W);
+      const int cnt = merge_row<NOPS>(P, W, (int)tot, 0);
       for (int t = lane; t < cnt; t += 32) {
         stg_stream(P.out_idx + dst + t, (int64_t)W.st_col[t]);
         stg_stream(P.out_vals + dst + t, W.st_val[t]);
@@ -628,7 +635,10 @@ template <typename ColT, typename Cfg>
 void launch_tiles(stamrt::Call& call, const SpaddParams& P, int64_t ntiles) {
   if (ntiles <= 0) return;
   const size_t smem = sizeof(TileSmem<ColT, Cfg>);
-  auto kern = spadd_tiles_kernel<ColT, Cfg>;
+  // operand counts specialised at compile time (loops unrolled)
+  auto kern = P.nops == 2 ? spadd_tiles_kernel<ColT, Cfg, 2>
+              : P.nops == 3 ? spadd_tiles_kernel<ColT, Cfg, 3>
+                            : spadd_tiles_kernel<ColT, Cfg, 0>;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   call.before_launch(sizeof(ColT) == 4 ? "spadd_tiles<u32>" : "spadd_tiles<i64>");
   kern<<<(unsigned)ntiles, Cfg::kWarps * 32, smem, call.stream()>>>(P);
