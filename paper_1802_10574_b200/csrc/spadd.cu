@@ -45,15 +45,24 @@ struct TileCfg {
   static constexpr int kTileRows = W * RPW;
   static constexpr int kStage = STAGE;
 };
+#ifndef SPADD_MIDTHRESH
+#define SPADD_MIDTHRESH 360
+#endif
 #ifndef SPADD_MID_WARPS
 #define SPADD_MID_WARPS 4
 #endif
 #ifndef SPADD_MID_STAGE
 #define SPADD_MID_STAGE 768
 #endif
-using ShortRows = TileCfg<8, 2, 384>;
+#ifndef SPADD_SHORT_W
+#define SPADD_SHORT_W 24
+#define SPADD_SHORT_RPW 1
+#define SPADD_SHORT_STAGE 256
+#endif
+using ShortRows = TileCfg<SPADD_SHORT_W, SPADD_SHORT_RPW, SPADD_SHORT_STAGE>;
+using MediumRows = TileCfg<16, 1, 384>;
 using MidRowsCfg = TileCfg<SPADD_MID_WARPS, 1, SPADD_MID_STAGE>;
-constexpr int kStageMin = 384;
+constexpr int kStageMin = SPADD_SHORT_STAGE < SPADD_MID_STAGE ? SPADD_SHORT_STAGE : SPADD_MID_STAGE;
 
 enum RowState : int { kStaged = 0, kPostponed = 1, kDeferred = 2 };
 
@@ -709,8 +718,12 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
       in_bytes += ops[p].nnz * 16;
     }
     // rows averaging a few hundred entries: one row per warp, deeper staging
-    const bool mid_rows = ncols <= (int64_t)UINT32_MAX && nrows > 0 && cap / nrows > 360;
-    const int64_t kTileRows = mid_rows ? MidRowsCfg::kTileRows : ShortRows::kTileRows;
+    // tile shape by the average row (sum over operands): rows fitting 256
+    // staged entries, 384, or longer (measured: profiles/r01_suite_spadd_k.csv)
+    const int64_t avg_row = nrows > 0 ? cap / nrows : 0;
+    const int shape = ncols > (int64_t)UINT32_MAX ? 0 : avg_row <= 224 ? 0 : avg_row <= SPADD_MIDTHRESH ? 1 : 2;
+    const int64_t kTileRows = shape == 0 ? ShortRows::kTileRows
+                              : shape == 1 ? MediumRows::kTileRows : MidRowsCfg::kTileRows;
     P.ntiles = ceil_div(nrows, kTileRows);
     const bool host_out = call.opts().result_mem == STAM_MEM_HOST;
     // Host operands or a host result: stream row blocks.  Block k's operand
@@ -779,8 +792,10 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
       P.block_end = marks ? marks + k : nullptr;
       P.tile_counter = reinterpret_cast<unsigned long long*>(ctl + 4 + k);
       if (ncols <= (int64_t)UINT32_MAX) {
-        if (mid_rows)
+        if (shape == 2)
           launch_tiles<uint32_t, MidRowsCfg>(call, P, t1 - t0);
+        else if (shape == 1)
+          launch_tiles<uint32_t, MediumRows>(call, P, t1 - t0);
         else
           launch_tiles<uint32_t, ShortRows>(call, P, t1 - t0);
       } else {
