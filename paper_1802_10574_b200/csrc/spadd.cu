@@ -114,23 +114,72 @@ struct TileSmem {
 // Number of elements < x (lower) or <= x (upper) in sorted s[0..n).
 // Branchless; trip count = bit length of n, uniform across a warp searching
 // one operand row.
-template <typename ColT>
-__device__ __forceinline__ int rank_lower(const ColT* s, int n, ColT x) {
+// The search depth (bit length of n) is warp-uniform: every lane searches the
+// same operand row.  A fall-through switch enters the fully unrolled steps at
+// that depth (no per-step loop control).
+#define STAM_RANK_STEP(B, CMP)                                    \
+  case (B) + 1: {                                                 \
+    const int probe = pos + (1 << (B));                           \
+    pos = (probe <= n && CMP(s[probe - 1], x)) ? probe : pos;     \
+  }                                                               \
+    [[fallthrough]];
+#define STAM_LT(a, b) ((a) < (b))
+#define STAM_LE(a, b) ((a) <= (b))
+template <bool kUpper, typename ColT>
+__device__ __forceinline__ int rank_of(const ColT* s, int n, ColT x) {
   int pos = 0;
-  for (int step = n ? (1 << (31 - __clz(n))) : 0; step > 0; step >>= 1) {
-    const int probe = pos + step;
-    pos = (probe <= n && s[probe - 1] < x) ? probe : pos;
+  const int depth = n ? 32 - __clz(n) : 0;  // steps 2^(depth-1) .. 1
+  if (depth > 12) {  // longer than any staging here: plain loop
+    for (int step = 1 << (depth - 1); step > 0; step >>= 1) {
+      const int probe = pos + step;
+      pos = (probe <= n && (kUpper ? s[probe - 1] <= x : s[probe - 1] < x)) ? probe : pos;
+    }
+    return pos;
+  }
+  if constexpr (kUpper) {
+    switch (depth) {
+      STAM_RANK_STEP(11, STAM_LE)
+      STAM_RANK_STEP(10, STAM_LE)
+      STAM_RANK_STEP(9, STAM_LE)
+      STAM_RANK_STEP(8, STAM_LE)
+      STAM_RANK_STEP(7, STAM_LE)
+      STAM_RANK_STEP(6, STAM_LE)
+      STAM_RANK_STEP(5, STAM_LE)
+      STAM_RANK_STEP(4, STAM_LE)
+      STAM_RANK_STEP(3, STAM_LE)
+      STAM_RANK_STEP(2, STAM_LE)
+      STAM_RANK_STEP(1, STAM_LE)
+      STAM_RANK_STEP(0, STAM_LE)
+      default:
+        break;
+    }
+  } else {
+    switch (depth) {
+      STAM_RANK_STEP(11, STAM_LT)
+      STAM_RANK_STEP(10, STAM_LT)
+      STAM_RANK_STEP(9, STAM_LT)
+      STAM_RANK_STEP(8, STAM_LT)
+      STAM_RANK_STEP(7, STAM_LT)
+      STAM_RANK_STEP(6, STAM_LT)
+      STAM_RANK_STEP(5, STAM_LT)
+      STAM_RANK_STEP(4, STAM_LT)
+      STAM_RANK_STEP(3, STAM_LT)
+      STAM_RANK_STEP(2, STAM_LT)
+      STAM_RANK_STEP(1, STAM_LT)
+      STAM_RANK_STEP(0, STAM_LT)
+      default:
+        break;
+    }
   }
   return pos;
 }
 template <typename ColT>
+__device__ __forceinline__ int rank_lower(const ColT* s, int n, ColT x) {
+  return rank_of<false>(s, n, x);
+}
+template <typename ColT>
 __device__ __forceinline__ int rank_upper(const ColT* s, int n, ColT x) {
-  int pos = 0;
-  for (int step = n ? (1 << (31 - __clz(n))) : 0; step > 0; step >>= 1) {
-    const int probe = pos + step;
-    pos = (probe <= n && s[probe - 1] <= x) ? probe : pos;
-  }
-  return pos;
+  return rank_of<true>(s, n, x);
 }
 
 __device__ __forceinline__ int64_t lower_bound_global(const int64_t* s, int64_t n, int64_t x) {
