@@ -18,6 +18,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -77,13 +78,18 @@ def build_cuda(verbose: bool = False, force: bool = False) -> Path:
     nvcc = _nvcc()
     objs = []
     hdrs = _headers()
+    jobs = []
     for src in CUDA_SOURCES:
         s = CSRC / src
         o = OBJ / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
             lang = ["-x", "cu"] if s.suffix == ".cpp" else []
-            _run([nvcc, *ARCH, *NVCC_FLAGS, *lang, "-c", str(s), "-o", str(o)], verbose)
+            jobs.append([nvcc, *ARCH, *NVCC_FLAGS, *lang, "-c", str(s), "-o", str(o)])
+    # translation units are independent: compile them concurrently
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, j, verbose) for j in jobs]:
+            f.result()
     out = LIB / "libstam_cuda.so"
     if force or _stale(out, objs):
         _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", str(out), *map(str, objs),

@@ -125,11 +125,11 @@ struct TileSmem {
     [[fallthrough]];
 #define STAM_LT(a, b) ((a) < (b))
 #define STAM_LE(a, b) ((a) <= (b))
-template <bool kUpper, typename ColT>
+template <bool kUpper, bool kSwitch, typename ColT>
 __device__ __forceinline__ int rank_of(const ColT* s, int n, ColT x) {
   int pos = 0;
   const int depth = n ? 32 - __clz(n) : 0;  // steps 2^(depth-1) .. 1
-  if (depth > 12) {  // longer than any staging here: plain loop
+  if (!kSwitch || depth > 12) {  // longer than any staging here: plain loop
     for (int step = 1 << (depth - 1); step > 0; step >>= 1) {
       const int probe = pos + step;
       pos = (probe <= n && (kUpper ? s[probe - 1] <= x : s[probe - 1] < x)) ? probe : pos;
@@ -173,13 +173,15 @@ __device__ __forceinline__ int rank_of(const ColT* s, int n, ColT x) {
   }
   return pos;
 }
-template <typename ColT>
+// kSwitch = false keeps the plain loop (generic operand counts: the unrolled
+// switch inside 16 x 16 operand loops would blow up code size).
+template <bool kSwitch = true, typename ColT>
 __device__ __forceinline__ int rank_lower(const ColT* s, int n, ColT x) {
-  return rank_of<false>(s, n, x);
+  return rank_of<false, kSwitch>(s, n, x);
 }
-template <typename ColT>
+template <bool kSwitch = true, typename ColT>
 __device__ __forceinline__ int rank_upper(const ColT* s, int n, ColT x) {
-  return rank_of<true>(s, n, x);
+  return rank_of<true, kSwitch>(s, n, x);
 }
 
 __device__ __forceinline__ int64_t lower_bound_global(const int64_t* s, int64_t n, int64_t x) {
@@ -245,9 +247,7 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
   uint8_t* st_op = W.st_op + out;
   // scatter every element to its merged slot
   bool dup = false;
-#pragma unroll
-  for (int o = 0; o < (NOPS ? NOPS : kMaxOps); o++) {
-    if (!NOPS && o >= nops) break;
+  auto scatter_operand = [&](int o) {
     const double* vsrc = P.vals[o] + W.seg_beg[o];
     const int len = W.seg_len[o];
     const int co = W.seg_co[o];
@@ -255,24 +255,35 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
       const double v = P.values ? ldg_stream(vsrc + t) : 0.0;
       const ColT x = W.in_col[co + t];
       int m = t;
-#pragma unroll
-      for (int q = 0; q < (NOPS ? NOPS : kMaxOps); q++) {
-        if (!NOPS && q >= nops) break;
-        if (q == o) continue;
+      auto rank_in = [&](int q) {
         const ColT* sq = W.in_col + W.seg_co[q];
         const int nq = W.seg_len[q];
         if (q < o) {
-          const int r = rank_upper(sq, nq, x);
+          const int r = rank_upper<NOPS != 0>(sq, nq, x);
           dup |= r > 0 && sq[r - 1] == x;
           m += r;
-        } else {
-          m += rank_lower(sq, nq, x);
+        } else if (q > o) {
+          m += rank_lower<NOPS != 0>(sq, nq, x);
         }
+      };
+      if constexpr (NOPS != 0) {
+#pragma unroll
+        for (int q = 0; q < NOPS; q++) rank_in(q);
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < nops; q++) rank_in(q);
       }
       st_col[m] = x;
       st_val[m] = v;
       st_op[m] = (uint8_t)o;
     }
+  };
+  if constexpr (NOPS != 0) {
+#pragma unroll
+    for (int o = 0; o < NOPS; o++) scatter_operand(o);
+  } else {
+#pragma unroll 1
+    for (int o = 0; o < nops; o++) scatter_operand(o);
   }
   __syncwarp();
   // no column in two operands: the merge is already the compact row
