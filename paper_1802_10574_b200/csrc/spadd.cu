@@ -236,6 +236,51 @@ __device__ __forceinline__ void load_cols(const SpaddParams& P, WarpStage<ColT, 
   __syncwarp();
 }
 
+// Combines runs of equal columns of the merged row st_*[out, out+L) in
+// operand order (assign, then accumulate: the workspace semantics) and
+// compacts in place.  any_dup (warp-uniform) false: nothing to combine.
+template <typename ColT, int STAGE>
+__device__ __forceinline__ int combine_staged(WarpStage<ColT, STAGE>& W, int L, int out, bool any_dup) {
+  const unsigned lane = lane_id();
+  ColT* st_col = W.st_col + out;
+  double* st_val = W.st_val + out;
+  const uint8_t* st_op = W.st_op + out;
+  __syncwarp();
+  // no column in two operands: the merge is already the compact row
+  if (!any_dup) return L;
+  // combine runs of equal columns in operand order; compact in place
+  int count = 0;
+  ColT prev = 0;
+  for (int base = 0; base < L; base += 32) {
+    const int m = base + (int)lane;
+    ColT x = 0;
+    double w = 0.0;
+    bool lead = false;
+    if (m < L) {
+      x = st_col[m];
+      const ColT before = (lane == 0) ? prev : st_col[m - 1];
+      lead = (m == 0) || (before != x);
+      if (lead) {
+        const double v0 = st_val[m];
+        w = (st_op[m] == 0) ? v0 : add_rn(0.0, v0);  // assign vs accumulate into 0.0
+        for (int n = m + 1; n < L && st_col[n] == x; n++) w = add_rn(w, st_val[n]);
+      }
+    }
+    prev = __shfl_sync(kFull, x, 31);
+    const unsigned lead_mask = __ballot_sync(kFull, lead);
+    const int slot = count + __popc(lead_mask & lanemask_lt());
+    __syncwarp();
+    if (lead) {
+      st_col[slot] = x;
+      st_val[slot] = w;
+    }
+    __syncwarp();
+    count += __popc(lead_mask);
+  }
+  return count;
+}
+
+
 // Rank-merge the staged row into st_* at [out, out+L) (operand order on ties),
 // then combine equal columns in place.  Returns the number of distinct columns.
 template <int NOPS, typename ColT, int STAGE>
@@ -285,39 +330,108 @@ __device__ int merge_row(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
 #pragma unroll 1
     for (int o = 0; o < nops; o++) scatter_operand(o);
   }
-  __syncwarp();
-  // no column in two operands: the merge is already the compact row
-  if (!__any_sync(kFull, dup)) return L;
-  // combine runs of equal columns in operand order; compact in place
-  int count = 0;
-  ColT prev = 0;
-  for (int base = 0; base < L; base += 32) {
-    const int m = base + (int)lane;
-    ColT x = 0;
-    double w = 0.0;
-    bool lead = false;
-    if (m < L) {
-      x = st_col[m];
-      const ColT before = (lane == 0) ? prev : st_col[m - 1];
-      lead = (m == 0) || (before != x);
-      if (lead) {
-        const double v0 = st_val[m];
-        w = (st_op[m] == 0) ? v0 : add_rn(0.0, v0);  // assign vs accumulate into 0.0
-        for (int n = m + 1; n < L && st_col[n] == x; n++) w = add_rn(w, st_val[n]);
-      }
-    }
-    prev = __shfl_sync(kFull, x, 31);
-    const unsigned lead_mask = __ballot_sync(kFull, lead);
-    const int slot = count + __popc(lead_mask & lanemask_lt());
-    __syncwarp();
-    if (lead) {
-      st_col[slot] = x;
-      st_val[slot] = w;
-    }
-    __syncwarp();
-    count += __popc(lead_mask);
+  return combine_staged(W, L, out, __any_sync(kFull, dup));
+}
+
+// ---------------------------------------------------------------------------
+// Padded rank-merge (specialised operand counts).  Operand q's columns are
+// staged at in_col[q*D, q*D + len_q) and padded with a sentinel above every
+// column up to D = 2^DLOG > every len_q, so a rank is exactly DLOG
+// branchless probes with no bounds test.  The row's elements are walked
+// flattened across operands (lane e -> operand o, index t), every lane
+// searching the NOPS-1 other operands: rank of x among operand q's columns
+// counts s < x for q > o and s <= x (= s < x + 1) for q < o, which puts equal
+// columns adjacent in operand order — the same merged position as merge_row.
+template <typename ColT>
+__device__ __forceinline__ ColT rank_sentinel() {
+  return sizeof(ColT) == 8 ? (ColT)0x7fffffffffffffffll : (ColT)0xffffffffu;
+}
+
+template <int NOPS, typename ColT, int STAGE>
+__device__ __forceinline__ void load_cols_padded(const SpaddParams& P, WarpStage<ColT, STAGE>& W,
+                                                 int D) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int q = 0; q < NOPS; q++) {
+    const int64_t* src = P.idx[q] + W.seg_beg[q];
+    const int len = W.seg_len[q];
+    ColT* dst = W.in_col + q * D;
+    for (int t = lane; t < D; t += 32) dst[t] = t < len ? (ColT)ldg_stream(src + t) : rank_sentinel<ColT>();
   }
-  return count;
+  __syncwarp();
+}
+
+template <int NOPS, int DLOG, typename ColT, int STAGE>
+__device__ __forceinline__ int merge_flat(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L) {
+  constexpr int D = 1 << DLOG;
+  const unsigned lane = lane_id();
+  int co[NOPS];
+  const double* vb[NOPS];
+#pragma unroll
+  for (int q = 0; q < NOPS; q++) {
+    co[q] = W.seg_co[q];
+    vb[q] = P.vals[q] + W.seg_beg[q];
+  }
+  bool dup = false;
+  for (int e = lane; e < L; e += 32) {
+    int o = 0;
+    int c0 = 0;
+    const double* vp = vb[0];
+#pragma unroll
+    for (int q = 1; q < NOPS; q++) {
+      const bool ge = e >= co[q];
+      o += ge;
+      c0 = ge ? co[q] : c0;
+      vp = ge ? vb[q] : vp;
+    }
+    const int t = e - c0;
+    const ColT x = W.in_col[o * D + t];
+    const double v = P.values ? ldg_stream(vp + t) : 0.0;
+    int m = t;
+#pragma unroll
+    for (int k = 1; k < NOPS; k++) {
+      int q = o + k;
+      q = q >= NOPS ? q - NOPS : q;
+      const bool upper = q < o;
+      const ColT xx = x + (ColT)upper;
+      const ColT* sq = W.in_col + q * D;
+      int r = 0;
+#pragma unroll
+      for (int b = DLOG - 1; b >= 0; b--) r = (sq[r + (1 << b) - 1] < xx) ? r + (1 << b) : r;
+      dup |= upper && r > 0 && sq[r - 1] == x;
+      m += r;
+    }
+    W.st_col[m] = x;
+    W.st_val[m] = v;
+    W.st_op[m] = (uint8_t)o;
+  }
+  return combine_staged(W, L, 0, __any_sync(kFull, dup));
+}
+
+// Stages and merges the row through the padded path when NOPS * D fits the
+// staging; returns -1 (nothing staged) otherwise.
+template <int NOPS, typename ColT, int STAGE>
+__device__ __forceinline__ int merge_row_padded(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L) {
+  if constexpr (NOPS == 2 || NOPS == 3) {
+    int maxlen = 0;
+#pragma unroll
+    for (int q = 0; q < NOPS; q++) maxlen = max(maxlen, W.seg_len[q]);
+    const int dlog = 32 - __clz(maxlen);  // D = 2^dlog > maxlen: a rank reaches len
+    if (dlog > 8 || (NOPS << dlog) > STAGE) return -1;
+    load_cols_padded<NOPS>(P, W, 1 << dlog);
+    switch (dlog) {
+      case 0: return merge_flat<NOPS, 0>(P, W, L);
+      case 1: return merge_flat<NOPS, 1>(P, W, L);
+      case 2: return merge_flat<NOPS, 2>(P, W, L);
+      case 3: return merge_flat<NOPS, 3>(P, W, L);
+      case 4: return merge_flat<NOPS, 4>(P, W, L);
+      case 5: return merge_flat<NOPS, 5>(P, W, L);
+      case 6: return merge_flat<NOPS, 6>(P, W, L);
+      case 7: return merge_flat<NOPS, 7>(P, W, L);
+      default: return merge_flat<NOPS, 8>(P, W, L);
+    }
+  }
+  return -1;
 }
 
 // Distinct-column count of a staged row (in_col only, no merge written).
@@ -407,7 +521,12 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     const int64_t tot = row_segments(S, W, nops, r);
     int64_t cnt;
     int state;
-    if (tot <= kStage - stage_off) {
+    int padded = -1;
+    if (stage_off == 0 && tot <= kStage) padded = merge_row_padded<NOPS>(P, W, (int)tot);
+    if (padded >= 0) {
+      cnt = padded;
+      state = kStaged;
+    } else if (tot <= kStage - stage_off) {
       load_cols<NOPS>(P, W);
       cnt = merge_row<NOPS>(P, W, (int)tot, stage_off);
       state = kStaged;
