@@ -340,60 +340,123 @@ __global__ void __launch_bounds__(256) mttkrp_dense_generic_kernel(const DensePa
   }
 }
 
-// Sums the partials of every slice cut by chunk boundaries, in a fixed order:
-// one CTA per chain (the chunk holding the slice's tail partial plus the
-// following chunks holding its head partials); 8 warps take strided chunks,
-// then the 8 warp sums are added in warp order (deterministic).
-constexpr int kFixThreads = 1024;
-__global__ void __launch_bounds__(kFixThreads) mttkrp_dense_fixup_kernel(const DenseParams P) {
-  __shared__ int64_t end_sh;
-  __shared__ double red[kFixThreads / 32][32];
+// Sums the partials of every slice cut by chunk boundaries, in a fixed order.
+// A chain = the chunk holding a slice's tail partial plus the following chunks
+// holding its head partials.  Most chains span 2-3 chunks; a heavy slice's
+// spans ~10^4, so two levels of block sums come first:
+//  * level 1: every aligned block of 32 chunks whose heads all belong to one
+//    slice (or are empty) gets its head partials summed in chunk order;
+//  * level 2: the same over aligned blocks of 32 level-1 blocks;
+//  * chains: a warp per chain walks forward from the tail partial, taking
+//    whole level-2 / level-1 blocks where they are aligned and uniform and
+//    loose chunks elsewhere, and sums the items in walk order (lane = column).
+// Every order is fixed by the chunking: results are deterministic run to run.
+constexpr int kFixBlock = 32;          // items per block sum (both levels)
+constexpr int64_t kSliceMixed = -1;    // head "none" / block not uniform
+constexpr int64_t kSliceEmpty = -2;    // empty chunk / block of empty chunks
+
+// One level of block sums.  Input item t has slice hs[t * hstride] and, for
+// column block cbi, values vals[cbi * vcb + t * vstride + lane].
+__global__ void mttkrp_dense_blocksum_kernel(const int64_t* hs, int hstride, const double* vals,
+                                             int64_t vstride, int64_t vcb, int64_t n, int64_t ncb,
+                                             double* bsum, int64_t* bslice, int64_t nblocks) {
   const int lane = (int)lane_id();
-  const int warp = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t task = warp; task < nblocks * ncb; task += nwarps) {
+    const int64_t b = task % nblocks, cbi = task / nblocks;
+    const int64_t t0 = b * kFixBlock;
+    const int64_t t = t0 + lane;
+    const int64_t h = t < n ? hs[t * hstride] : kSliceEmpty;
+    const unsigned nonempty = __ballot_sync(kFull, h != kSliceEmpty);
+    int64_t sb = kSliceEmpty;
+    if (nonempty) sb = __shfl_sync(kFull, h, __ffs(nonempty) - 1);
+    const bool full = __all_sync(kFull, h == kSliceEmpty || h == sb) && sb != kSliceMixed;
+    if (cbi == 0 && lane == 0) bslice[b] = full ? sb : kSliceMixed;
+    if (!full || sb == kSliceEmpty) continue;
+    const double* base = vals + cbi * vcb;
+    double v[kFixBlock];
+#pragma unroll
+    for (int u = 0; u < kFixBlock; u++)
+      v[u] = ((nonempty >> u) & 1) ? base[(t0 + u) * vstride + lane] : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int u = 0; u < kFixBlock; u++) sum += v[u];
+    bsum[(cbi * nblocks + b) * 32 + lane] = sum;
+  }
+}
+
+struct FixupLevels {
+  const double* bsum1;
+  const int64_t* bslice1;
+  int64_t nb1;
+  const double* bsum2;
+  const int64_t* bslice2;
+  int64_t nb2;
+};
+
+// Sums the leading run of items (lanes 0..) whose slice is s or empty, in
+// order; returns the run length.  `lim` caps the items examined.
+__device__ __forceinline__ int take_items(const int64_t* hs, int hstride, const double* vals,
+                                          int64_t vstride, int64_t t0, int lim, int64_t s,
+                                          double& acc) {
+  const int lane = (int)lane_id();
+  const int64_t h = lane < lim ? hs[(t0 + lane) * hstride] : kSliceMixed;
+  const bool ok = lane < lim && (h == s || h == kSliceEmpty);
+  const unsigned bad = __ballot_sync(kFull, !ok);
+  const int run = bad ? __ffs(bad) - 1 : 32;
+  const unsigned take = __ballot_sync(kFull, ok && h == s) & (run == 32 ? kFull : ((1u << run) - 1));
+  for (int u0 = 0; u0 < run; u0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      v[u] = (u0 + u < run && ((take >> (u0 + u)) & 1)) ? vals[(t0 + u0 + u) * vstride + lane] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (u0 + u < run && ((take >> (u0 + u)) & 1)) acc += v[u];
+  }
+  return run;
+}
+
+__global__ void mttkrp_dense_fixup_kernel(const DenseParams P, const FixupLevels L) {
+  const int lane = (int)lane_id();
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t ncb = (P.R + 31) / 32;
-  for (int64_t c = blockIdx.x; c < P.nchunks; c += gridDim.x) {
+  constexpr int64_t kB2 = (int64_t)kFixBlock * kFixBlock;
+  for (int64_t c = warp; c < P.nchunks; c += nwarps) {
     const int64_t s = P.part_slice[2 * c + 1];
-    if (s < 0) continue;  // uniform across the CTA
-    // chain end: first chunk after c whose head is neither s nor an empty chunk
-    if (threadIdx.x == 0) end_sh = P.nchunks;
-    __syncthreads();
-    for (int64_t base = c + 1; base < P.nchunks; base += kFixThreads) {
-      const int64_t t = base + threadIdx.x;
-      if (t < P.nchunks) {
-        const int64_t h = P.part_slice[2 * t];
-        if (h != s && h != -2) atomicMin((long long*)&end_sh, (long long)t);
-      }
-      __syncthreads();
-      if (end_sh < P.nchunks) break;
-    }
-    const int64_t e = end_sh;
+    if (s < 0) continue;  // uniform across the warp
     for (int64_t cbi = 0; cbi < ncb; cbi++) {
       const double* base = P.part + cbi * P.nchunks * 64;
-      // 4 independent partial loads in flight per lane (order fixed per warp)
-      double sum = 0.0;
-      constexpr int kW = kFixThreads / 32;
-      int64_t c2 = c + 1 + warp;
-      for (; c2 + 3 * kW < e; c2 += 4 * kW) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int64_t cc = c2 + u * kW;
-          v[u] = P.part_slice[2 * cc] == s ? base[(cc * 2) * 32 + lane] : 0.0;
+      double acc = base[(c * 2 + 1) * 32 + lane];
+      int64_t t = c + 1;
+      while (t < P.nchunks) {
+        if (t % kB2 == 0 && t / kB2 < L.nb2) {
+          const int64_t b = t / kB2;
+          const int lim = (int)min((int64_t)32, L.nb2 - b);
+          const int run = take_items(L.bslice2, 1, L.bsum2 + cbi * L.nb2 * 32, 32, b, lim, s, acc);
+          t += (int64_t)run * kB2;
+          if (run == lim && lim == 32) continue;
+          if (run == lim) { if (t >= P.nchunks) break; }
         }
-#pragma unroll
-        for (int u = 0; u < 4; u++) sum += v[u];
+        if (t % kFixBlock == 0 && t / kFixBlock < L.nb1) {
+          const int64_t b = t / kFixBlock;
+          // up to the next level-2 boundary
+          const int64_t bend = min(L.nb1, (b / kFixBlock + 1) * kFixBlock);
+          const int lim = (int)(bend - b);
+          const int run = take_items(L.bslice1, 1, L.bsum1 + cbi * L.nb1 * 32, 32, b, lim, s, acc);
+          t += (int64_t)run * kFixBlock;
+          if (run == lim) continue;
+        }
+        // loose chunks up to the next level-1 boundary
+        const int lim = (int)(min(P.nchunks, (t / kFixBlock + 1) * kFixBlock) - t);
+        const int run = take_items(P.part_slice, 2, base, 64, t, lim, s, acc);
+        t += run;
+        if (run < lim) break;  // the chain ends at chunk t
       }
-      for (; c2 < e; c2 += kW)
-        if (P.part_slice[2 * c2] == s) sum += base[(c2 * 2) * 32 + lane];
-      red[warp][lane] = sum;
-      __syncthreads();
-      if (warp == 0) {
-        double total = base[(c * 2 + 1) * 32 + lane];
-        for (int w = 0; w < kFixThreads / 32; w++) total += red[w][lane];
-        const int64_t col = cbi * 32 + lane;
-        if (col < P.R) P.A[s * P.R + col] = total;
-      }
-      __syncthreads();
+      const int64_t col = cbi * 32 + lane;
+      if (col < P.R) P.A[s * P.R + col] = acc;
     }
   }
 }
@@ -834,9 +897,28 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       else
         mttkrp_dense_generic_kernel<<<(unsigned)(sms * 4), 256, 0, call.stream()>>>(P);
       call.after_launch();
+      FixupLevels L{};
+      L.nb1 = ceil_div(P.nchunks, (int64_t)kFixBlock);
+      L.nb2 = ceil_div(L.nb1, (int64_t)kFixBlock);
+      double* bsum1 = call.scratch_n<double>((size_t)(ncb * L.nb1 * 32));
+      int64_t* bslice1 = call.scratch_n<int64_t>((size_t)L.nb1);
+      double* bsum2 = call.scratch_n<double>((size_t)(ncb * L.nb2 * 32));
+      int64_t* bslice2 = call.scratch_n<int64_t>((size_t)L.nb2);
+      L.bsum1 = bsum1;
+      L.bslice1 = bslice1;
+      L.bsum2 = bsum2;
+      L.bslice2 = bslice2;
+      call.before_launch("mttkrp_dense_blocksum");
+      mttkrp_dense_blocksum_kernel<<<(unsigned)std::min<int64_t>(ceil_div(L.nb1 * ncb, 8), (int64_t)sms * 8),
+                                     256, 0, call.stream()>>>(P.part_slice, 2, P.part, 64, P.nchunks * 64,
+                                                              P.nchunks, ncb, bsum1, bslice1, L.nb1);
+      mttkrp_dense_blocksum_kernel<<<(unsigned)std::min<int64_t>(ceil_div(L.nb2 * ncb, 8), (int64_t)sms * 8),
+                                     256, 0, call.stream()>>>(bslice1, 1, bsum1, 32, L.nb1 * 32, L.nb1, ncb,
+                                                              bsum2, bslice2, L.nb2);
+      call.after_launch();
       call.before_launch("mttkrp_dense_fixup");
-      mttkrp_dense_fixup_kernel<<<(unsigned)std::min<int64_t>(P.nchunks, (int64_t)sms * 8),
-                                  kFixThreads, 0, call.stream()>>>(P);
+      mttkrp_dense_fixup_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(P.nchunks, 8), (int64_t)sms * 8)),
+                                  256, 0, call.stream()>>>(P, L);
       call.after_launch();
     }
     call.finish_dense_result(A);
