@@ -373,42 +373,51 @@ struct SlotMap {
   }
 };
 
-// Column span of row i from the first/last column of every B row it touches.
+// Column span of row i from the first/last column of every B row it touches
+// (columns < 2^32: the tables hold 32-bit keys).
 __device__ SlotMap row_slot_map(const SpgemmParams& P, int64_t a0, int na, int total, int tb,
                                 int64_t* red) {
-  int64_t lo = INT64_MAX, hi = -1;
+  unsigned lo = 0xffffffffu, hi = 0u;
+  bool any = false;
   for (int p = threadIdx.x; p < na; p += blockDim.x) {
     const int o = P.aoff[a0 + p];
     const int e = (p + 1 < na) ? P.aoff[a0 + p + 1] : total;
     if (e > o) {
       const int64_t b0 = P.bst[a0 + p];
-      lo = min(lo, P.bidx[b0]);
-      hi = max(hi, P.bidx[b0 + (e - o) - 1]);
+      lo = min(lo, (unsigned)P.bidx[b0]);
+      hi = max(hi, (unsigned)P.bidx[b0 + (e - o) - 1]);
+      any = true;
     }
   }
-  lo = -warp_max(-lo);
-  hi = warp_max(hi);
+  lo = __reduce_min_sync(kFull, lo);
+  hi = __reduce_max_sync(kFull, hi);
+  any = __any_sync(kFull, any);
+  unsigned* r32 = reinterpret_cast<unsigned*>(red);
   if (blockDim.x == 32) {
     if (threadIdx.x == 0) {
-      red[0] = lo;
-      red[1] = hi;
+      r32[0] = lo;
+      r32[1] = any ? hi : 0u;
+      r32[2] = any;
     }
     __syncwarp();
   } else {
     if (threadIdx.x == 0) {
-      red[0] = INT64_MAX;
-      red[1] = -1;
+      r32[0] = 0xffffffffu;
+      r32[1] = 0u;
+      r32[2] = 0u;
     }
     __syncthreads();
-    if (lane_id() == 0) {
-      atomicMin((long long*)&red[0], (long long)lo);
-      atomicMax((long long*)&red[1], (long long)hi);
+    if (lane_id() == 0 && any) {
+      atomicMin(&r32[0], lo);
+      atomicMax(&r32[1], hi);
+      r32[2] = 1u;
     }
     __syncthreads();
   }
   SlotMap sm;
-  sm.c0 = red[0];
-  const uint64_t span = red[1] >= red[0] ? (uint64_t)(red[1] - red[0] + 1) : 1;
+  const bool nonempty = r32[2] != 0;
+  sm.c0 = nonempty ? (int64_t)r32[0] : 0;
+  const uint64_t span = nonempty ? (uint64_t)(r32[1] - r32[0]) + 1 : 1;
   sm.scale = ((uint64_t)tb << 32) / span;
   if (sm.scale == 0) sm.scale = 1;
   return sm;
@@ -454,9 +463,8 @@ struct HashKeysSmem {
 };
 
 __device__ __forceinline__ int row_table(int64_t prod) {
-  int tb = 64;
-  while (tb < 2 * prod) tb <<= 1;
-  return tb;
+  const int need = (int)(2 * prod);  // next power of two >= 2P, at least 64
+  return need <= 64 ? 64 : 1 << (32 - __clz(need - 1));
 }
 
 template <int THREADS>
@@ -484,13 +492,19 @@ __device__ __forceinline__ int64_t claim_row(unsigned long long* claim, int64_t*
   return r;
 }
 
+// CTA total of one int per thread; `sh` is zero on entry and left zero for
+// the next call (the caller's next CTA barrier orders the reset).
 template <int THREADS>
 __device__ __forceinline__ int cta_sum(int v, int* sh) {
   if constexpr (THREADS == 32) {
     return warp_sum(v);
   } else {
-    int tot;
-    block_exclusive_scan(v, sh, &tot);
+    v = warp_sum(v);
+    if (lane_id() == 0 && v) atomicAdd(sh, v);
+    __syncthreads();
+    const int tot = *sh;
+    __syncthreads();
+    if (threadIdx.x == 0) *sh = 0;
     return tot;
   }
 }
@@ -619,12 +633,13 @@ __device__ void drain_table(const uint32_t* keys, const double* vals, int nslots
 }
 
 template <int THREADS, int TB>
-__global__ void __launch_bounds__(THREADS) hash_symbolic_kernel(const SpgemmParams P,
+__global__ void __launch_bounds__(THREADS, (THREADS >= 64 ? 2048 / THREADS : 32)) hash_symbolic_kernel(const SpgemmParams P,
                                                                  const int64_t* rows,
                                                                  int64_t nrows,
                                                                  unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   HashKeysSmem<TB>& S = *reinterpret_cast<HashKeysSmem<TB>*>(smem_raw);
+  if (threadIdx.x == 0) S.scan[0] = 0;  // cta_sum's accumulator (claim_row syncs)
   while (true) {
     const int64_t r = claim_row<THREADS>(claim, &S.claimed);
     if (r >= nrows) break;
