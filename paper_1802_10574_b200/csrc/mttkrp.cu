@@ -257,6 +257,154 @@ __global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParam
   }
 }
 
+// R == 32, quarter-warp per fiber: a warp walks a chunk's fibers four at a
+// time, quarter q (8 lanes, 4 columns each: two 16-byte loads per row) owns
+// fiber f4 + q.  Short fibers (the median fiber holds one nonzero) thus put
+// four D rows and four C rows in flight per warp step instead of one; long
+// fibers stream their nonzeros in batches of 8 per quarter (coalesced k/b
+// loads, 4 row loads in flight per lane).  Each quarter keeps w0 for its
+// fiber; w0 * C(j,:) accumulates into the quarter's share of the slice row,
+// and the four shares are combined (xor shuffles, fixed order) when the slice
+// is flushed.  Slice/partial bookkeeping is the same as mttkrp_dense32.
+__global__ void __launch_bounds__(256, 2) mttkrp_dense32q_kernel(const DenseParams P) {
+  const int lane = (int)lane_id();
+  const int q = lane >> 3;
+  const int col = 4 * (lane & 7);
+  const int qbase = lane & ~7;
+  while (true) {
+    int64_t c = 0;
+    if (lane == 0) c = (int64_t)atomicAdd(P.counter, 1ull);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= P.nchunks) break;
+    const int64_t fa = P.chunk_fa[c], fb = P.chunk_fa[c + 1];
+    double* part = P.part + (c * 2) * 32;
+    if (fa >= fb) {
+      if (lane == 0) {
+        P.part_slice[2 * c] = -2;
+        P.part_slice[2 * c + 1] = -1;
+      }
+      continue;
+    }
+    SliceTracker st;
+    st.s = P.chunk_s[c];
+    st.s_end = P.pos1[st.s + 1];
+    st.open = P.pos1[st.s] < fa;
+    st.wrote_head = false;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    auto flush = [&](bool ends_here) {
+      double t[4];
+#pragma unroll
+      for (int x = 0; x < 4; x++) {
+        t[x] = acc[x] + __shfl_xor_sync(kFull, acc[x], 8);
+        t[x] += __shfl_xor_sync(kFull, t[x], 16);
+        acc[x] = 0.0;
+      }
+      const bool started_here = !st.open;
+      double* dst;
+      if (started_here && ends_here) {
+        dst = P.A + st.s * 32 + col;
+      } else {
+        const int slot = started_here ? 1 : 0;
+        dst = part + slot * 32 + col;
+        if (lane == 0) P.part_slice[2 * c + slot] = st.s;
+        if (slot == 0) st.wrote_head = true;
+      }
+      if (q == 0) {
+        reinterpret_cast<double2*>(dst)[0] = make_double2(t[0], t[1]);
+        reinterpret_cast<double2*>(dst)[1] = make_double2(t[2], t[3]);
+      }
+    };
+    for (int64_t fg = fa; fg < fb; fg += 32) {
+      const int nf = (int)min((int64_t)32, fb - fg);
+      int mj = 0, mlen = 0;
+      int64_t mz = 0;
+      if (lane < nf) {
+        mj = (int)P.idx1[fg + lane];
+        mz = P.pos2[fg + lane];
+        mlen = (int)(P.pos2[fg + lane + 1] - mz);
+      }
+      for (int g = 0; g < nf; g += 4) {
+        const int src = g + q;
+        const bool fv = src < nf;
+        const int64_t z0 = __shfl_sync(kFull, mz, src & 31);
+        const int len_s = __shfl_sync(kFull, mlen, src & 31);  // every lane shuffles
+        const int len = fv ? len_s : 0;
+        const int j = __shfl_sync(kFull, mj, src & 31);
+        double2 c0 = make_double2(0.0, 0.0), c1 = c0;
+        if (fv) {
+          const double2* cr = reinterpret_cast<const double2*>(P.C + (int64_t)j * 32 + col);
+          c0 = __ldg(cr);
+          c1 = __ldg(cr + 1);
+        }
+        const int nmax = __reduce_max_sync(kFull, (unsigned)len);
+        double w[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int zb = 0; zb < nmax; zb += 8) {
+          // lane (q, l) loads nonzero zb + l of its quarter's fiber
+          int kk = 0;
+          double bb = 0.0;
+          const int zl = zb + (lane & 7);
+          if (zl < len) {
+            kk = (int)P.idx2[z0 + zl];
+            bb = P.vals[z0 + zl];
+          }
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            if (zb + 4 * h >= nmax) break;  // uniform
+            double2 d[4][2];
+            double b[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const int uu = 4 * h + u;
+              const int k = __shfl_sync(kFull, kk, qbase + uu);
+              const double bv = __shfl_sync(kFull, bb, qbase + uu);
+              const bool ok = zb + uu < len;
+              b[u] = ok ? bv : 0.0;
+              if (ok) {
+                const double2* dr = reinterpret_cast<const double2*>(P.D + (int64_t)k * 32 + col);
+                d[u][0] = __ldg(dr);
+                d[u][1] = __ldg(dr + 1);
+              } else {
+                d[u][0] = make_double2(0.0, 0.0);
+                d[u][1] = d[u][0];
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              w[0] = fma(b[u], d[u][0].x, w[0]);
+              w[1] = fma(b[u], d[u][0].y, w[1]);
+              w[2] = fma(b[u], d[u][1].x, w[2]);
+              w[3] = fma(b[u], d[u][1].y, w[3]);
+            }
+          }
+        }
+        // fibers g..g+3 in order: add the owner quarter's share, flush at slice ends
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (g + u >= nf) break;  // uniform
+          const int64_t f = fg + g + u;
+          while (f >= st.s_end) {
+            st.s++;
+            st.s_end = P.pos1[st.s + 1];
+            st.open = false;
+          }
+          if (q == u) {
+            acc[0] = fma(w[0], c0.x, acc[0]);
+            acc[1] = fma(w[1], c0.y, acc[1]);
+            acc[2] = fma(w[2], c1.x, acc[2]);
+            acc[3] = fma(w[3], c1.y, acc[3]);
+          }
+          if (f + 1 == st.s_end) flush(true);
+        }
+      }
+    }
+    if (fb < st.s_end) flush(false);
+    if (lane == 0) {
+      if (!st.wrote_head) P.part_slice[2 * c] = -1;
+      if (!(fb < st.s_end && !st.open)) P.part_slice[2 * c + 1] = -1;
+    }
+  }
+}
+
 // Any R: column blocks of 32, a full warp per nonzero, one double per lane.
 __global__ void __launch_bounds__(256) mttkrp_dense_generic_kernel(const DenseParams P) {
   const int lane = (int)lane_id();
@@ -893,7 +1041,7 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       call.after_launch();
       call.before_launch(fast ? "mttkrp_dense32" : "mttkrp_dense_generic");
       if (fast)
-        mttkrp_dense32_kernel<<<(unsigned)(sms * 3), 256, 0, call.stream()>>>(P);
+        mttkrp_dense32q_kernel<<<(unsigned)(sms * 2), 256, 0, call.stream()>>>(P);
       else
         mttkrp_dense_generic_kernel<<<(unsigned)(sms * 4), 256, 0, call.stream()>>>(P);
       call.after_launch();
