@@ -323,6 +323,17 @@ __global__ void __launch_bounds__(256, 2) mttkrp_dense32q_kernel(const DensePara
         mz = P.pos2[fg + lane];
         mlen = (int)(P.pos2[fg + lane + 1] - mz);
       }
+      // first batch (8 nonzeros per quarter) of step 0, then one step ahead
+      int pk = 0;
+      double pb = 0.0;
+      {
+        const int64_t z0n = __shfl_sync(kFull, mz, q);
+        const int lenn = __shfl_sync(kFull, mlen, q);
+        if (q < nf && (lane & 7) < lenn) {
+          pk = (int)P.idx2[z0n + (lane & 7)];
+          pb = P.vals[z0n + (lane & 7)];
+        }
+      }
       for (int g = 0; g < nf; g += 4) {
         const int src = g + q;
         const bool fv = src < nf;
@@ -336,16 +347,32 @@ __global__ void __launch_bounds__(256, 2) mttkrp_dense32q_kernel(const DensePara
           c0 = __ldg(cr);
           c1 = __ldg(cr + 1);
         }
+        int kk = pk;
+        double bb = pb;
+        if (g + 4 < nf) {  // uniform: prefetch the next step's first batch
+          const int src2 = g + 4 + q;
+          const int64_t z0n = __shfl_sync(kFull, mz, src2 & 31);
+          const int lenn = __shfl_sync(kFull, mlen, src2 & 31);
+          pk = 0;
+          pb = 0.0;
+          if (src2 < nf && (lane & 7) < lenn) {
+            pk = (int)P.idx2[z0n + (lane & 7)];
+            pb = P.vals[z0n + (lane & 7)];
+          }
+        }
         const int nmax = __reduce_max_sync(kFull, (unsigned)len);
         double w[4] = {0.0, 0.0, 0.0, 0.0};
         for (int zb = 0; zb < nmax; zb += 8) {
-          // lane (q, l) loads nonzero zb + l of its quarter's fiber
-          int kk = 0;
-          double bb = 0.0;
-          const int zl = zb + (lane & 7);
-          if (zl < len) {
-            kk = (int)P.idx2[z0 + zl];
-            bb = P.vals[z0 + zl];
+          // lane (q, l) holds nonzero zb + l of its quarter's fiber; load the
+          // next batch before consuming this one
+          int kn = 0;
+          double bn = 0.0;
+          if (zb + 8 < nmax) {
+            const int zl = zb + 8 + (lane & 7);
+            if (zl < len) {
+              kn = (int)P.idx2[z0 + zl];
+              bn = P.vals[z0 + zl];
+            }
           }
 #pragma unroll
           for (int h = 0; h < 2; h++) {
@@ -376,6 +403,8 @@ __global__ void __launch_bounds__(256, 2) mttkrp_dense32q_kernel(const DensePara
               w[3] = fma(b[u], d[u][1].y, w[3]);
             }
           }
+          kk = kn;
+          bb = bn;
         }
         // fibers g..g+3 in order: add the owner quarter's share, flush at slice ends
 #pragma unroll
