@@ -266,7 +266,10 @@ __global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParam
 // fiber; w0 * C(j,:) accumulates into the quarter's share of the slice row,
 // and the four shares are combined (xor shuffles, fixed order) when the slice
 // is flushed.  Slice/partial bookkeeping is the same as mttkrp_dense32.
-__global__ void __launch_bounds__(256, 2) mttkrp_dense32q_kernel(const DenseParams P) {
+#ifndef DQ_MINB
+#define DQ_MINB 2
+#endif
+__global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const DenseParams P) {
   const int lane = (int)lane_id();
   const int q = lane >> 3;
   const int col = 4 * (lane & 7);
@@ -1070,7 +1073,7 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       call.after_launch();
       call.before_launch(fast ? "mttkrp_dense32" : "mttkrp_dense_generic");
       if (fast)
-        mttkrp_dense32q_kernel<<<(unsigned)(sms * 2), 256, 0, call.stream()>>>(P);
+        mttkrp_dense32q_kernel<<<(unsigned)(sms * DQ_MINB), 256, 0, call.stream()>>>(P);
       else
         mttkrp_dense_generic_kernel<<<(unsigned)(sms * 4), 256, 0, call.stream()>>>(P);
       call.after_launch();
