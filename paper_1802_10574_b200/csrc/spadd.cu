@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -950,6 +952,21 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     int64_t* marks = host_out ? call.marks() : nullptr;
 
     std::vector<cudaEvent_t> done((size_t)nblocks);
+    // STAM_DEBUG_STREAM=1: per-block timeline (copy done, kernel done, d2h done) on stderr
+    const bool dbg = std::getenv("STAM_DEBUG_STREAM") != nullptr;
+    struct TlPoint {
+      std::chrono::steady_clock::time_point t;
+      std::string name;
+    };
+    static std::vector<TlPoint*> tl;
+    auto mark_n = [&](cudaStream_t st, std::string n) {
+      if (!dbg) return;
+      auto* p = new TlPoint{{}, std::move(n)};
+      tl.push_back(p);
+      STAM_CUDA_CHECK(cudaLaunchHostFunc(
+          st, [](void* u) { static_cast<TlPoint*>(u)->t = std::chrono::steady_clock::now(); }, p));
+    };
+    mark_n(call.stream(), "start");
     auto issue_block = [&](int64_t k) {
       const int64_t t0 = blk[(size_t)k];
       const int64_t t1 = blk[(size_t)k + 1];
@@ -965,6 +982,7 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
                             (size_t)(e1 - e0) * sizeof(double));
         }
         call.wait(call.copy_fence());
+        mark_n(call.ctx()->copy_stream, "h2d " + std::to_string(k));
       }
       P.tile_base = t0;
       P.last_tile = t1 - 1;
@@ -980,6 +998,7 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
       } else {
         launch_tiles<int64_t, ShortRows>(call, P, t1 - t0);
       }
+      mark_n(call.stream(), "kern " + std::to_string(k));
       if (host_out) {
         done[(size_t)k] = call.event();
         STAM_CUDA_CHECK(cudaEventRecord(done[(size_t)k], call.stream()));
@@ -1002,6 +1021,7 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
                        (size_t)(r1 - r0 + (k == 0 ? 1 : 0)) * sizeof(int64_t), done[(size_t)k]);
         call.d2h_range(h_idx + prev, D->idx + prev, (size_t)(end - prev) * sizeof(int64_t), nullptr);
         call.d2h_range(h_vals + prev, D->vals + prev, (size_t)(end - prev) * sizeof(double), nullptr);
+        mark_n(call.ctx()->d2h_stream, "d2h " + std::to_string(k) + " " + std::to_string((end - prev) >> 10) + "K");
         prev = end;
         if (issued < nblocks) issue_block(issued++);
       }
@@ -1024,6 +1044,15 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     int64_t tail[2];
     call.read_scalars(reinterpret_cast<const int64_t*>(ctl), 2, tail);  // deferred, total
     const int64_t nnz = tail[1];
+    if (dbg) {
+      STAM_CUDA_CHECK(cudaDeviceSynchronize());
+      for (auto* q : tl) {
+        const double ms = std::chrono::duration<double, std::milli>(q->t - tl[0]->t).count();
+        fprintf(stderr, "[spadd] %8.3f ms  %s\n", ms, q->name.c_str());
+      }
+      for (auto* q : tl) delete q;
+      tl.clear();
+    }
     if (host_out) {
       if (tail[0] > 0) {
         // long rows were filled after their blocks came down (the stream
