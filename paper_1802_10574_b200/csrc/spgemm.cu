@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 64 ? 2048 / THREADS : 32)
 }
 
 template <int THREADS, int TB>
-__global__ void __launch_bounds__(THREADS) hash_numeric_kernel(const SpgemmParams P,
+__global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 ? 32 : 1536 / THREADS)) hash_numeric_kernel(const SpgemmParams P,
                                                                 const int64_t* rows,
                                                                 int64_t nrows,
                                                                 unsigned long long* claim) {
