@@ -12,13 +12,13 @@
 // B200 design:
 //  dense  — the nonzeros are cut into fiber-aligned chunks of ~equal nnz (so
 //           the power-law i-slices, one holding 38% of the nnz, spread over
-//           the whole GPU); a warp walks a chunk's fibers; the w0 row lives in
-//           registers, two half-warps take alternate nonzeros and read D rows
-//           with 128-bit loads (R = 32: one row = 16 lanes x double2); at the
-//           fiber end w0 * C(j,:) is accumulated per slice.  Slices inside a
-//           chunk are stored directly; slices cut by chunk boundaries leave
-//           per-chunk partials that a second kernel sums in chunk order
-//           (deterministic; no atomics on the heavy slices).
+//           the whole GPU); a warp walks a chunk's fibers four at a time, a
+//           quarter-warp per fiber (R = 32: one row = 8 lanes x 32 B) with its
+//           w0 share in registers; at the fiber end w0 * C(j,:) is accumulated
+//           into the quarter's share of the slice row.  Slices inside a chunk
+//           are stored directly; slices cut by chunk boundaries leave
+//           per-chunk partials that block sums and a warp per chain add in a
+//           fixed order (deterministic; no atomics on the heavy slices).
 //  sparse — a warp per slice (claimed dynamically), lanes over fibers; per
 //           fiber, w0 is evaluated only at C_j's stored coordinates
 //           (presence-checked; the C_j and D_k column ids are held in
@@ -106,157 +106,6 @@ struct SliceTracker {
   bool wrote_head;
 };
 
-// R == 32 with 16-byte aligned rows: two half-warps take alternate nonzeros
-// of a fiber and read D rows as double2 (a row = 16 lanes x 16 B); up to 8
-// independent row loads in flight per lane; the next fiber's first (k, b)
-// batch and its C row are issued before the current fiber is reduced.
-__global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParams P) {
-  const int lane = (int)lane_id();
-  const int half = lane >> 4;
-  const int col = 2 * (lane & 15);
-  while (true) {
-    int64_t c = 0;
-    if (lane == 0) c = (int64_t)atomicAdd(P.counter, 1ull);
-    c = __shfl_sync(kFull, c, 0);
-    if (c >= P.nchunks) break;
-    const int64_t fa = P.chunk_fa[c], fb = P.chunk_fa[c + 1];
-    double* part = P.part + (c * 2) * 32;
-    if (fa >= fb) {
-      if (lane == 0) {
-        P.part_slice[2 * c] = -2;
-        P.part_slice[2 * c + 1] = -1;
-      }
-      continue;
-    }
-    SliceTracker st;
-    st.s = P.chunk_s[c];
-    st.s_end = P.pos1[st.s + 1];
-    st.open = P.pos1[st.s] < fa;
-    st.wrote_head = false;
-    double acc0 = 0.0, acc1 = 0.0;
-    auto flush = [&](bool ends_here) {
-      const bool started_here = !st.open;
-      if (started_here && ends_here) {
-        if (half == 0)
-          reinterpret_cast<double2*>(P.A + st.s * 32 + col)[0] = make_double2(acc0, acc1);
-      } else {
-        const int slot = started_here ? 1 : 0;
-        if (half == 0) reinterpret_cast<double2*>(part + slot * 32 + col)[0] = make_double2(acc0, acc1);
-        if (lane == 0) P.part_slice[2 * c + slot] = st.s;
-        if (slot == 0) st.wrote_head = true;
-      }
-      acc0 = 0.0;
-      acc1 = 0.0;
-    };
-    for (int64_t fg = fa; fg < fb; fg += 32) {
-      const int nf = (int)min((int64_t)32, fb - fg);
-      int64_t mj = 0, mz = 0, mz1 = 0;
-      if (lane < nf) {
-        mj = P.idx1[fg + lane];
-        mz = P.pos2[fg + lane];
-        mz1 = P.pos2[fg + lane + 1];
-      }
-      // first batch of fiber 0 of the group
-      int64_t z0 = __shfl_sync(kFull, mz, 0);
-      int64_t z1 = __shfl_sync(kFull, mz1, 0);
-      int kz = 0;
-      double bz = 0.0;
-      if (lane < z1 - z0) {
-        kz = (int)P.idx2[z0 + lane];
-        bz = P.vals[z0 + lane];
-      }
-      int64_t jn = __shfl_sync(kFull, mj, 0);
-      double2 cj = __ldg(reinterpret_cast<const double2*>(P.C + jn * 32 + col));
-      for (int t = 0; t < nf; t++) {
-        const int64_t f = fg + t;
-        while (f >= st.s_end) {
-          st.s++;
-          st.s_end = P.pos1[st.s + 1];
-          st.open = false;
-        }
-        const int64_t cz0 = z0, cz1 = z1;
-        int ckz = kz;
-        double cbz = bz;
-        const double2 ccj = cj;
-        // prefetch the next fiber's first batch and C row
-        if (t + 1 < nf) {
-          z0 = __shfl_sync(kFull, mz, t + 1);
-          z1 = __shfl_sync(kFull, mz1, t + 1);
-          kz = 0;
-          bz = 0.0;
-          if (lane < z1 - z0) {
-            kz = (int)P.idx2[z0 + lane];
-            bz = P.vals[z0 + lane];
-          }
-          jn = __shfl_sync(kFull, mj, t + 1);
-          cj = __ldg(reinterpret_cast<const double2*>(P.C + jn * 32 + col));
-        }
-        double w0 = 0.0, w1 = 0.0;
-        for (int64_t zb = cz0; zb < cz1; zb += 32) {
-          const int n = (int)min((int64_t)32, cz1 - zb);
-          if (zb != cz0) {
-            ckz = 0;
-            cbz = 0.0;
-            if (lane < n) {
-              ckz = (int)P.idx2[zb + lane];
-              cbz = P.vals[zb + lane];
-            }
-          }
-          int t0 = 0;
-          for (; t0 + 8 < n; t0 += 16) {  // 16 nonzeros: 8 independent row loads per lane
-            double2 d[8];
-            double b[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-              const int src = t0 + 2 * u + half;
-              const int k = __shfl_sync(kFull, ckz, src & 31);
-              const double bv = __shfl_sync(kFull, cbz, src & 31);
-              const bool ok = src < n;
-              b[u] = ok ? bv : 0.0;
-              d[u] = ok ? __ldg(reinterpret_cast<const double2*>(P.D + (int64_t)k * 32 + col))
-                        : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-              w0 = fma(b[u], d[u].x, w0);
-              w1 = fma(b[u], d[u].y, w1);
-            }
-          }
-          if (t0 < n) {  // tail of at most 8 nonzeros (most fibers are short)
-            double2 d[4];
-            double b[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const int src = t0 + 2 * u + half;
-              const int k = __shfl_sync(kFull, ckz, src & 31);
-              const double bv = __shfl_sync(kFull, cbz, src & 31);
-              const bool ok = src < n;
-              b[u] = ok ? bv : 0.0;
-              d[u] = ok ? __ldg(reinterpret_cast<const double2*>(P.D + (int64_t)k * 32 + col))
-                        : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              w0 = fma(b[u], d[u].x, w0);
-              w1 = fma(b[u], d[u].y, w1);
-            }
-          }
-        }
-        w0 += __shfl_xor_sync(kFull, w0, 16);
-        w1 += __shfl_xor_sync(kFull, w1, 16);
-        acc0 = fma(w0, ccj.x, acc0);
-        acc1 = fma(w1, ccj.y, acc1);
-        if (f + 1 == st.s_end) flush(true);
-      }
-    }
-    if (fb < st.s_end) flush(false);
-    if (lane == 0) {
-      if (!st.wrote_head) P.part_slice[2 * c] = -1;
-      if (!(fb < st.s_end && !st.open)) P.part_slice[2 * c + 1] = -1;
-    }
-  }
-}
-
 // R == 32, quarter-warp per fiber: a warp walks a chunk's fibers four at a
 // time, quarter q (8 lanes, 4 columns each: two 16-byte loads per row) owns
 // fiber f4 + q.  Short fibers (the median fiber holds one nonzero) thus put
@@ -265,7 +114,8 @@ __global__ void __launch_bounds__(256, 3) mttkrp_dense32_kernel(const DenseParam
 // loads, 4 row loads in flight per lane).  Each quarter keeps w0 for its
 // fiber; w0 * C(j,:) accumulates into the quarter's share of the slice row,
 // and the four shares are combined (xor shuffles, fixed order) when the slice
-// is flushed.  Slice/partial bookkeeping is the same as mttkrp_dense32.
+// is flushed.  Slice/partial bookkeeping: slices inside a chunk are stored directly, a
+// slice cut by a chunk boundary leaves a head or tail partial (SliceTracker).
 #ifndef DQ_MINB
 #define DQ_MINB 2
 #endif
