@@ -39,6 +39,7 @@ Call::~Call() {
     cudaStreamSynchronize(ctx_->copy_stream);
   }
   if (d2h_open_) cudaStreamSynchronize(ctx_->d2h_stream);
+  if (aux_open_) cudaStreamSynchronize(ctx_->aux_stream);
   for (void* p : temps_) cudaFreeAsync(p, ctx_->stream);
   if (!finished_) cudaStreamSynchronize(ctx_->stream);
 }
@@ -104,9 +105,27 @@ cudaEvent_t Call::copy_fence() {
   return ev;
 }
 
+cudaStream_t Call::fork() {
+  if (!ctx_->aux_stream)
+    STAM_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx_->aux_stream, cudaStreamNonBlocking));
+  cudaEvent_t ev = event();
+  STAM_CUDA_CHECK(cudaEventRecord(ev, ctx_->stream));
+  STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->aux_stream, ev, 0));
+  aux_open_ = true;
+  return ctx_->aux_stream;
+}
+
+void Call::join() {
+  if (!aux_open_) return;
+  aux_open_ = false;
+  cudaEvent_t ev = event();
+  STAM_CUDA_CHECK(cudaEventRecord(ev, ctx_->aux_stream));
+  STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->stream, ev, 0));
+}
+
 void Call::wait(cudaEvent_t ev) { STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->stream, ev, 0)); }
 
-void Call::before_launch(const char* name) {
+void Call::before_launch(const char* name, cudaStream_t st) {
   stats_->kernel_launches++;
   if (!opts_.timing) return;
   if (ctx_->event_next + 2 > ctx_->event_pool.size()) {
@@ -118,15 +137,15 @@ void Call::before_launch(const char* name) {
   }
   TimedLaunch t{name, ctx_->event_pool[ctx_->event_next], ctx_->event_pool[ctx_->event_next + 1]};
   ctx_->event_next += 2;
-  STAM_CUDA_CHECK(cudaEventRecord(t.start, ctx_->stream));
+  STAM_CUDA_CHECK(cudaEventRecord(t.start, st ? st : ctx_->stream));
   launches_.push_back(t);
   pending_ = (int)launches_.size() - 1;
 }
 
-void Call::after_launch() {
+void Call::after_launch(cudaStream_t st) {
   STAM_CUDA_CHECK(cudaGetLastError());
   if (!opts_.timing || pending_ < 0) return;
-  STAM_CUDA_CHECK(cudaEventRecord(launches_[pending_].stop, ctx_->stream));
+  STAM_CUDA_CHECK(cudaEventRecord(launches_[pending_].stop, st ? st : ctx_->stream));
   pending_ = -1;
 }
 
@@ -475,6 +494,7 @@ int stam_cuda_ctx_destroy(stam_cuda_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     if (ctx->h_marks) cudaFreeHost(ctx->h_marks);
     delete ctx;
   });

@@ -48,6 +48,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // host->device staging overlapped with kernels
   cudaStream_t d2h_stream = nullptr;   // device->host result blocks overlapped with kernels
+  cudaStream_t aux_stream = nullptr;   // bandwidth-bound kernels overlapped with compute-bound ones
   // pinned, device-mapped marks written by kernels (e.g. a row block's end
   // offset) and read by the host after the block's event
   int64_t* h_marks = nullptr;
@@ -108,8 +109,13 @@ class Call {
   cudaEvent_t event();
 
   // Launch bookkeeping: call before/after each kernel launch.
-  void before_launch(const char* name);
-  void after_launch();
+  void before_launch(const char* name, cudaStream_t st = nullptr);
+  void after_launch(cudaStream_t st = nullptr);
+  // Second kernel stream: fork() orders it after the main stream's work so
+  // far and returns it; join() orders the main stream after it (before the
+  // call's temporaries are released).
+  cudaStream_t fork();
+  void join();
 
   // Read one int64 from device memory (synchronizes the stream).
   int64_t read_scalar(const int64_t* dptr);
@@ -151,6 +157,7 @@ class Call {
   bool finished_ = false;
   bool copies_open_ = false;
   bool d2h_open_ = false;
+  bool aux_open_ = false;
   int pending_ = -1;
 };
 

@@ -26,7 +26,8 @@
 //      long P > 4096          : 1024-thread CTA per row (rows claimed longest
 //                                 first), a column bitmap over all columns in
 //                                 shared memory (popcount rank) and fp64
-//                                 atomics into the pre-assembled output row.
+//                                 atomics; computed once, before the scan,
+//                                 into a scratch region, then copied into C.
 //  * products are enumerated flattened, warp-contiguous and lane-interleaved
 //    (B rows read coalesced), with 4 independent gathers in flight per lane.
 #include <cub/device/device_radix_sort.cuh>
@@ -726,36 +727,20 @@ __device__ __forceinline__ void set_bit(unsigned long long* bits, int64_t col) {
   atomicOr(&bits[col >> 6], 1ull << (col & 63));
 }
 
-__global__ void __launch_bounds__(kLongThreads) long_symbolic_kernel(const SpgemmParams P,
-                                                                     const int64_t* rows,
-                                                                     int64_t nrows,
-                                                                     unsigned long long* claim) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  LongHeader& S = *reinterpret_cast<LongHeader*>(smem_raw);
-  auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
-  const int nw = (int)((P.n + 63) >> 6);
-  while (true) {
-    const int64_t r = claim_row<kLongThreads>(claim, &S.claimed);
-    if (r >= nrows) break;
-    const int64_t i = rows[r];
-    for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
-    __syncthreads();
-    const int64_t a0 = P.apos[i];
-    for_products<false>(P, a0, (int)(P.apos[i + 1] - a0), (int)P.prod[i],
-                        [&](int64_t col, double) { set_bit(bits, col); });
-    __syncthreads();
-    int cnt = 0;
-    for (int w = threadIdx.x; w < nw; w += blockDim.x) cnt += __popcll(bits[w]);
-    int tot;
-    block_exclusive_scan(cnt, S.scan, &tot);
-    if (threadIdx.x == 0) P.cpos[i + 1] = tot;
-  }
-}
-
+// Long rows in one pass, before the row-pointer scan: the row's column
+// bitmap, an exclusive popcount prefix per word, the sorted column list and
+// the values (fp64 atomics at each product's popcount slot) go to a scratch
+// region at the row's products offset (an upper bound of its output), and
+// the exact count to cpos[i+1].  After the scan long_copy_kernel moves the
+// rows into C.  (Replaces a symbolic bitmap pass + a numeric bitmap pass:
+// the products are enumerated twice instead of three times.)
 __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const SpgemmParams P,
                                                                     const int64_t* rows,
                                                                     int64_t nrows,
-                                                                    unsigned long long* claim) {
+                                                                    unsigned long long* claim,
+                                                                    const int64_t* soff,
+                                                                    uint32_t* sidx,
+                                                                    double* sval) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LongHeader& S = *reinterpret_cast<LongHeader*>(smem_raw);
   auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
@@ -765,11 +750,8 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
     const int64_t r = claim_row<kLongThreads>(claim, &S.claimed);
     if (r >= nrows) break;
     const int64_t i = rows[r];
-    const int64_t dst = P.cpos[i];
-    const int64_t cnt = P.cpos[i + 1] - dst;
+    const int64_t dst = soff[r];
     for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
-    if (P.values)
-      for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) P.cvals[dst + t] = 0.0;
     __syncthreads();
     const int64_t a0 = P.apos[i];
     const int na = (int)(P.apos[i + 1] - a0);
@@ -778,6 +760,7 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
     __syncthreads();
     // exclusive popcount prefix per word and the sorted column list: warp w
     // owns words [w*per_w, (w+1)*per_w), lane-interleaved in 32-word chunks
+    int cnt;
     {
       const int lane = (int)lane_id();
       const int warp = threadIdx.x >> 5;
@@ -792,8 +775,10 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
         const int v = S.scan[lane];
         const int inc = warp_inclusive_scan(v);
         S.scan[lane] = inc - v;
+        if (lane == 31) S.scan[32] = inc;
       }
       __syncthreads();
+      cnt = S.scan[32];
       int run = S.scan[warp];
       for (int w = ww0; w < ww1; w += 32) {
         const int wl = w + lane;
@@ -805,21 +790,61 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
         unsigned long long mm = bm;
         while (mm) {
           const int b = __ffsll((long long)mm) - 1;
-          P.cidx[dst + pos] = (int64_t)wl * 64 + b;
+          sidx[dst + pos] = (uint32_t)(wl * 64 + b);
           pos++;
           mm &= mm - 1;
         }
         run += __shfl_sync(kFull, inc, 31);
       }
     }
+    if (threadIdx.x == 0) P.cpos[i + 1] = cnt;
+    if (P.values) {
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) sval[dst + t] = 0.0;
+      __syncthreads();
+      for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
+        const int w = (int)(col >> 6);
+        const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
+        atomicAdd(&sval[dst + slot], v);
+      });
+    }
     __syncthreads();
-    if (P.values)
-    for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
-      const int w = (int)(col >> 6);
-      const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
-      atomicAdd(&P.cvals[dst + slot], v);
-    });
-    __syncthreads();
+  }
+}
+
+// Long rows from their scratch regions into C: CTA per row (rows arrive
+// longest first), 4 independent loads in flight per thread.
+constexpr int kCopyThreads = 1024;
+__global__ void __launch_bounds__(kCopyThreads) long_copy_kernel(const SpgemmParams P,
+                                                                 const int64_t* rows,
+                                                                 int64_t nrows,
+                                                                 const int64_t* soff,
+                                                                 const uint32_t* sidx,
+                                                                 const double* sval) {
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int64_t dst = P.cpos[i], cnt = P.cpos[i + 1] - dst, src = soff[r];
+    for (int64_t base = 0; base < cnt; base += 4 * kCopyThreads) {
+      uint32_t c[4];
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t t = base + u * kCopyThreads + threadIdx.x;
+        c[u] = 0;
+        v[u] = 0.0;
+        if (t < cnt) {
+          c[u] = __ldcs(sidx + src + t);
+          if (P.values) v[u] = __ldcs(sval + src + t);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t t = base + u * kCopyThreads + threadIdx.x;
+        if (t < cnt) {
+          __stcs(reinterpret_cast<long long*>(P.cidx) + dst + t, (long long)c[u]);
+          if (P.values) __stcs(P.cvals + dst + t, v[u]);
+        }
+      }
+    }
   }
 }
 
@@ -839,16 +864,55 @@ void launch_hash(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows,
   call.after_launch();
 }
 
-void launch_long(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
-                 bool numeric, unsigned long long* claim) {
-  if (n == 0) return;
-  const size_t smem = long_smem_bytes(P.n, numeric);
-  auto kern = numeric ? long_numeric_kernel : long_symbolic_kernel;
-  STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t grid = std::min<int64_t>(n, call.ctx()->num_sms);
-  call.before_launch(numeric ? "spgemm_long_numeric" : "spgemm_long_symbolic");
-  kern<<<(unsigned)grid, kLongThreads, smem, call.stream()>>>(P, rows, n, claim);
+// Long rows: scratch offsets (products prefix over the long rows), the
+// one-pass kernel into scratch (before the scan) — returns the scratch.
+__global__ void gather_prod_kernel(const int64_t* rows, int64_t n, const int64_t* prod,
+                                   int64_t* out);
+
+struct LongScratch {
+  int64_t* soff = nullptr;
+  uint32_t* sidx = nullptr;
+  double* sval = nullptr;
+};
+
+LongScratch launch_long(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
+                        unsigned long long* claim) {
+  LongScratch L;
+  if (n == 0) return L;
+  L.soff = call.scratch_n<int64_t>((size_t)n + 1);
+  call.before_launch("spgemm_long_offsets");
+  gather_prod_kernel<<<(unsigned)stamrt::ceil_div(n, 256), 256, 0, call.stream()>>>(rows, n, P.prod,
+                                                                                  L.soff);
   call.after_launch();
+  STAM_CUDA_CHECK(cudaMemsetAsync(L.soff + n, 0, sizeof(int64_t), call.stream()));
+  size_t sb = 0;
+  STAM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, sb, L.soff, L.soff, n + 1, call.stream()));
+  void* stmp = call.scratch(sb);
+  STAM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(stmp, sb, L.soff, L.soff, n + 1, call.stream()));
+  const int64_t tot = call.read_scalar(L.soff + n);
+  L.sidx = call.scratch_n<uint32_t>((size_t)std::max<int64_t>(tot, 1));
+  if (P.values) L.sval = call.scratch_n<double>((size_t)std::max<int64_t>(tot, 1));
+  const size_t smem = long_smem_bytes(P.n, true);
+  STAM_CUDA_CHECK(cudaFuncSetAttribute(long_numeric_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = std::min<int64_t>(n, call.ctx()->num_sms);
+  call.before_launch("spgemm_long_numeric");
+  long_numeric_kernel<<<(unsigned)grid, kLongThreads, smem, call.stream()>>>(P, rows, n, claim,
+                                                                             L.soff, L.sidx, L.sval);
+  call.after_launch();
+  return L;
+}
+
+// The copy is bandwidth-bound and the hash numeric tiers are not: it runs on
+// the auxiliary stream, overlapped with them (the caller joins before the end).
+void launch_long_copy(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
+                      const LongScratch& L) {
+  if (n == 0) return;
+  cudaStream_t aux = call.fork();
+  call.before_launch("spgemm_long_copy", aux);
+  long_copy_kernel<<<(unsigned)std::min<int64_t>(n, (int64_t)call.ctx()->num_sms * 2), kCopyThreads,
+                     0, aux>>>(P, rows, n, L.soff, L.sidx, L.sval);
+  call.after_launch(aux);
 }
 
 template <int G>
@@ -1094,7 +1158,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], false, "spgemm_hashL1_symbolic", claims + 10);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
-    launch_long(call, P, rows_b[kBinLong], counts[kBinLong], false, claims + 4);
+    const LongScratch lsc = launch_long(call, P, rows_b[kBinLong], counts[kBinLong], claims + 4);
 
     // scan counts -> row pointers
     size_t temp_bytes = 0;
@@ -1114,6 +1178,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     P.cvals = Cr->vals;
     if (!P.values && nnz > 0)  // ASSEMBLE: index only, values defined as zero
       STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
+    launch_long_copy(call, P, rows_b[kBinLong], counts[kBinLong], lsc);
     // numeric (ASSEMBLE: the same passes without values)
     launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], true);
     launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], true);
@@ -1123,7 +1188,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
-    launch_long(call, P, rows_b[kBinLong], counts[kBinLong], true, claims + 9);
+    call.join();
 
     call.finish_csr_result(Cr, nnz);
     call.finish();
