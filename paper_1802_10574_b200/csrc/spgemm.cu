@@ -83,6 +83,10 @@ struct SpgemmParams {
   const int64_t* bidx;
   const double* bvals;
   int64_t* prod;             // [m] products per row
+  uint2* span;               // [m] first/last column any of the row's B rows holds (x > y: none)
+  uint2* bspan;              // [nrows(B)] first/last column of each B row (x > y: empty)
+  int64_t* arows;            // rows with more than kLongA entries (rowprod_long_kernel)
+  unsigned long long* narows;  // [0] their count, [1] claim counter
   int* aoff;                 // [nnz(A)] row-local product offset of each A entry
   int64_t* bst;              // [nnz(A)] start of the entry's B row
   unsigned long long* bins;  // [kNumBins] counts, then cursors
@@ -96,8 +100,45 @@ struct SpgemmParams {
 };
 
 // ---------------------------------------------------------------------------
-// rowprod: lane per row (32 rows in flight per warp); rows with more than 64
-// A entries are walked cooperatively by the warp.
+// rowprod: a warp takes 32 consecutive rows and walks their A entries flat,
+// 32 at a time (coalesced A reads, independent B-row gathers in every lane);
+// the row of an entry comes from a shuffle search over the 32 row starts, and
+// segmented warp scans give each entry its row-local product offset and each
+// row its products and column span.  Rows continuing past a window of 32
+// entries carry their partial sums into the next window.  Rows with more than
+// kLongA entries are skipped here and listed for rowprod_long_kernel (a warp
+// per row, claimed dynamically), so no warp is stuck behind a power-law row.
+constexpr int kLongA = 64;
+
+struct RowTally {
+  unsigned long long* hist;  // shared [kNumBins]
+  unsigned long long total = 0, maxp = 0;
+  __device__ void add(const SpgemmParams& P, int64_t row, int64_t s, unsigned lo, unsigned hi) {
+    P.prod[row] = s;
+    P.span[row] = make_uint2(lo, hi);
+    atomicAdd(&hist[bin_of(s)], 1ull);
+    total += (unsigned long long)s;
+    maxp = max(maxp, (unsigned long long)s);
+  }
+};
+
+__device__ __forceinline__ void tally_flush(const SpgemmParams& P, RowTally& T,
+                                            unsigned long long* sh_total,
+                                            unsigned long long* sh_max) {
+  const unsigned long long t = warp_sum(T.total);
+  const unsigned long long mx = warp_max(T.maxp);
+  if (lane_id() == 0) {
+    if (t) atomicAdd(sh_total, t);
+    atomicMax(sh_max, mx);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumBins && T.hist[threadIdx.x]) atomicAdd(&P.bins[threadIdx.x], T.hist[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    if (*sh_total) atomicAdd((unsigned long long*)&P.stats[0], *sh_total);
+    atomicMax((unsigned long long*)&P.stats[1], *sh_max);
+  }
+}
+
 __global__ void rowprod_kernel(const SpgemmParams P) {
   __shared__ unsigned long long hist[kNumBins];
   __shared__ unsigned long long total, maxp;
@@ -107,65 +148,159 @@ __global__ void rowprod_kernel(const SpgemmParams P) {
   const unsigned lane = lane_id();
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long local_total = 0, local_max = 0;
+  RowTally T;
+  T.hist = hist;
   for (int64_t base = warp * 32; base < P.m; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    int64_t s = 0, a0 = 0, a1 = 0;
-    if (i < P.m) {
-      a0 = P.apos[i];
-      a1 = P.apos[i + 1];
+    const int nr = (int)min((int64_t)32, P.m - base);
+    // lane l < nr: start of row base + l; lanes >= nr: the window's end
+    const int64_t rp = P.apos[base + min((int)lane, nr)];
+    const int64_t wend = P.apos[base + nr];
+    const int64_t wbeg = __shfl_sync(kFull, rp, 0);
+    int64_t rnx = __shfl_down_sync(kFull, rp, 1);  // end of row base + l
+    if (lane == 31) rnx = wend;
+    const bool mine = (int)lane < nr;
+    if (mine && rp == rnx) T.add(P, base + lane, 0, 0xffffffffu, 0u);
+    const bool longa = mine && rnx - rp > kLongA;
+    const unsigned lm = __ballot_sync(kFull, longa);
+    if (lm) {
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(&P.narows[0], (unsigned long long)__popc(lm));
+      at = __shfl_sync(kFull, at, 0);
+      if (longa) P.arows[at + __popc(lm & lanemask_lt())] = base + lane;
     }
-    const bool longrow = a1 - a0 > 64;
-    if (!longrow) {
-#pragma unroll 4
-      for (int64_t p = a0; p < a1; p++) {
-        const int64_t k = P.aidx[p];
-        const int64_t b0 = P.bpos[k];
-        P.bst[p] = b0;
-        P.aoff[p] = (int)s;
-        s += P.bpos[k + 1] - b0;
+    int carry_r = -1;
+    int64_t carry_s = 0;
+    unsigned carry_lo = 0xffffffffu, carry_hi = 0u;
+    int64_t c = wbeg;
+    while (c < wend) {
+      const int64_t p = c + lane;
+      // row of entry p: the largest r < nr with start(r) <= p
+      int r = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int cand = r + st;
+        const int64_t v = __shfl_sync(kFull, rp, cand & 31);
+        if (cand < nr && v <= p) r = cand;
       }
+      const int64_t rend = __shfl_sync(kFull, rnx, r);
+      const bool rlong = ((lm >> r) & 1u) != 0;
+      // a window position inside a listed row: jump past it
+      const int r0 = __shfl_sync(kFull, r, 0);
+      if ((lm >> r0) & 1u) {
+        c = __shfl_sync(kFull, rend, 0);
+        continue;
+      }
+      const bool valid = p < wend && !rlong;
+      int64_t len = 0;
+      unsigned lo = 0xffffffffu, hi = 0u;
+      if (valid) {
+        const int64_t k = P.aidx[p];
+        const int64_t b0 = P.bpos[k], b1 = P.bpos[k + 1];
+        const uint2 sp = P.bspan[k];
+        P.bst[p] = b0;
+        len = b1 - b0;
+        lo = sp.x;
+        hi = sp.y;
+      }
+      // segmented inclusive scans (a row's entries are contiguous lanes)
+      int64_t inc = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(kFull, inc, o);
+        const unsigned ul = __shfl_up_sync(kFull, lo, o), uh = __shfl_up_sync(kFull, hi, o);
+        const int ru = __shfl_up_sync(kFull, r, o);
+        if ((int)lane >= o && ru == r) {
+          inc += u;
+          lo = min(lo, ul);
+          hi = max(hi, uh);
+        }
+      }
+      const bool cont = r == carry_r;
+      const int64_t off = cont ? carry_s : 0;
+      if (valid) P.aoff[p] = (int)(off + inc - len);
+      const int64_t tot = off + inc;
+      if (cont) {
+        lo = min(lo, carry_lo);
+        hi = max(hi, carry_hi);
+      }
+      if (valid && p == rend - 1) T.add(P, base + r, tot, lo, hi);
+      const int lastv = (int)min((int64_t)31, wend - 1 - c);  // last in-window lane (uniform)
+      carry_r = __shfl_sync(kFull, r, lastv);
+      carry_s = __shfl_sync(kFull, tot, lastv);
+      carry_lo = __shfl_sync(kFull, lo, lastv);
+      carry_hi = __shfl_sync(kFull, hi, lastv);
+      c += 32;
     }
-    unsigned pending = __ballot_sync(kFull, longrow);
-    while (pending) {
-      const int src = __ffs(pending) - 1;
-      pending &= pending - 1;
-      const int64_t b0 = __shfl_sync(kFull, a0, src), b1 = __shfl_sync(kFull, a1, src);
-      int64_t carry = 0;
-      for (int64_t c = b0; c < b1; c += 32) {
-        const int64_t p = c + lane;
-        int64_t len = 0;
+  }
+  tally_flush(P, T, &total, &maxp);
+}
+
+// First/last column of every B row (8 bytes per row, L2-resident for rowprod's
+// gathers instead of two 32-byte sectors of B's column array per A entry).
+__global__ void bspan_kernel(const SpgemmParams P, int64_t nb) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nb;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = P.bpos[r], b1 = P.bpos[r + 1];
+    P.bspan[r] = b1 > b0 ? make_uint2((unsigned)P.bidx[b0], (unsigned)P.bidx[b1 - 1])
+                         : make_uint2(0xffffffffu, 0u);
+  }
+}
+
+// Rows with more than kLongA entries: a warp per row, claimed dynamically.
+__global__ void rowprod_long_kernel(const SpgemmParams P) {
+  __shared__ unsigned long long hist[kNumBins];
+  __shared__ unsigned long long total, maxp;
+  if (threadIdx.x < kNumBins) hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) total = maxp = 0;
+  __syncthreads();
+  const unsigned lane = lane_id();
+  RowTally T;
+  T.hist = hist;
+  const unsigned long long n = P.narows[0];
+  while (true) {
+    unsigned long long q = 0;
+    if (lane == 0) q = atomicAdd(&P.narows[1], 1ull);
+    q = __shfl_sync(kFull, q, 0);
+    if (q >= n) break;
+    const int64_t i = P.arows[q];
+    const int64_t b0 = P.apos[i], b1 = P.apos[i + 1];
+    int64_t carry = 0;
+    unsigned wlo = 0xffffffffu, whi = 0u;
+    constexpr int U = 8;  // 256 entries per step: all gathers issued before the scans
+    for (int64_t c = b0; c < b1; c += 32 * U) {
+      int64_t bs[U], len[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t p = c + 32 * u + lane;
+        bs[u] = 0;
+        len[u] = 0;
         if (p < b1) {
           const int64_t k = P.aidx[p];
-          const int64_t bs = P.bpos[k];
-          len = P.bpos[k + 1] - bs;
-          P.bst[p] = bs;
+          bs[u] = P.bpos[k];
+          len[u] = P.bpos[k + 1] - bs[u];
+          const uint2 sp = P.bspan[k];
+          wlo = min(wlo, sp.x);
+          whi = max(whi, sp.y);
         }
-        const int64_t inc = warp_inclusive_scan(len);
-        if (p < b1) P.aoff[p] = (int)(carry + inc - len);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t p = c + 32 * u + lane;
+        if (p < b1) P.bst[p] = bs[u];
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t p = c + 32 * u + lane;
+        const int64_t inc = warp_inclusive_scan(len[u]);
+        if (p < b1) P.aoff[p] = (int)(carry + inc - len[u]);
         carry += __shfl_sync(kFull, inc, 31);
       }
-      if ((int)lane == src) s = carry;
     }
-    if (i < P.m) {
-      P.prod[i] = s;
-      atomicAdd(&hist[bin_of(s)], 1ull);
-      local_total += (unsigned long long)s;
-      local_max = max(local_max, (unsigned long long)s);
-    }
+    wlo = __reduce_min_sync(kFull, wlo);
+    whi = __reduce_max_sync(kFull, whi);
+    if (lane == 0) T.add(P, i, carry, wlo, whi);
   }
-  local_total = warp_sum(local_total);
-  local_max = warp_max(local_max);
-  if (lane == 0) {
-    if (local_total) atomicAdd(&total, local_total);
-    atomicMax(&maxp, local_max);
-  }
-  __syncthreads();
-  if (threadIdx.x < kNumBins && hist[threadIdx.x]) atomicAdd(&P.bins[threadIdx.x], hist[threadIdx.x]);
-  if (threadIdx.x == 0) {
-    if (total) atomicAdd((unsigned long long*)&P.stats[0], total);
-    atomicMax((unsigned long long*)&P.stats[1], maxp);
-  }
+  tally_flush(P, T, &total, &maxp);
 }
 
 __global__ void bin_scatter_kernel(const SpgemmParams P, const unsigned long long* offsets) {
@@ -374,51 +509,14 @@ struct SlotMap {
   }
 };
 
-// Column span of row i from the first/last column of every B row it touches
-// (columns < 2^32: the tables hold 32-bit keys).
-__device__ SlotMap row_slot_map(const SpgemmParams& P, int64_t a0, int na, int total, int tb,
-                                int64_t* red) {
-  unsigned lo = 0xffffffffu, hi = 0u;
-  bool any = false;
-  for (int p = threadIdx.x; p < na; p += blockDim.x) {
-    const int o = P.aoff[a0 + p];
-    const int e = (p + 1 < na) ? P.aoff[a0 + p + 1] : total;
-    if (e > o) {
-      const int64_t b0 = P.bst[a0 + p];
-      lo = min(lo, (unsigned)P.bidx[b0]);
-      hi = max(hi, (unsigned)P.bidx[b0 + (e - o) - 1]);
-      any = true;
-    }
-  }
-  lo = __reduce_min_sync(kFull, lo);
-  hi = __reduce_max_sync(kFull, hi);
-  any = __any_sync(kFull, any);
-  unsigned* r32 = reinterpret_cast<unsigned*>(red);
-  if (blockDim.x == 32) {
-    if (threadIdx.x == 0) {
-      r32[0] = lo;
-      r32[1] = any ? hi : 0u;
-      r32[2] = any;
-    }
-    __syncwarp();
-  } else {
-    if (threadIdx.x == 0) {
-      r32[0] = 0xffffffffu;
-      r32[1] = 0u;
-      r32[2] = 0u;
-    }
-    __syncthreads();
-    if (lane_id() == 0 && any) {
-      atomicMin(&r32[0], lo);
-      atomicMax(&r32[1], hi);
-      r32[2] = 1u;
-    }
-    __syncthreads();
-  }
+// Order-preserving slot map of row i from its column span (computed by
+// rowprod from the first/last column of every B row the row touches).
+__device__ __forceinline__ SlotMap row_slot_map(const SpgemmParams& P, int64_t i, int tb) {
+  const uint2 sp = P.span[i];
   SlotMap sm;
-  const bool nonempty = r32[2] != 0;
-  sm.c0 = nonempty ? (int64_t)r32[0] : 0;
-  const uint64_t span = nonempty ? (uint64_t)(r32[1] - r32[0]) + 1 : 1;
+  const bool nonempty = sp.x <= sp.y;
+  sm.c0 = nonempty ? (int64_t)sp.x : 0;
+  const uint64_t span = nonempty ? (uint64_t)(sp.y - sp.x) + 1 : 1;
   sm.scale = ((uint64_t)tb << 32) / span;
   if (sm.scale == 0) sm.scale = 1;
   return sm;
@@ -650,7 +748,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 64 ? 2048 / THREADS : 32)
     const int nslots = tb + tb / 2;
     const int64_t a0 = P.apos[i];
     const int na = (int)(P.apos[i + 1] - a0);
-    const SlotMap sm = row_slot_map(P, a0, na, total, tb, S.red);
+    const SlotMap sm = row_slot_map(P, i, tb);
     for (int s = threadIdx.x; s < nslots; s += THREADS) S.keys[s] = kEmpty;
     cta_sync<THREADS>();
     int created = 0;
@@ -682,7 +780,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 
     const int nslots = tb + tb / 2;
     const int64_t a0 = P.apos[i];
     const int na = (int)(P.apos[i + 1] - a0);
-    const SlotMap sm = row_slot_map(P, a0, na, total, tb, S.red);
+    const SlotMap sm = row_slot_map(P, i, tb);
     for (int s = threadIdx.x; s < nslots; s += THREADS) {
       S.keys[s] = kEmpty;
       if (P.values) S.vals[s] = 0.0;
@@ -1057,6 +1155,7 @@ void prepare(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
   P.bidx = call.device_input(B->idx, (size_t)B->nnz, B->mem);
   P.bvals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
   P.prod = call.scratch_n<int64_t>((size_t)m);
+  P.span = call.scratch_n<uint2>((size_t)m);
   P.aoff = call.scratch_n<int>((size_t)std::max<int64_t>(A->nnz, 1));
   P.bst = call.scratch_n<int64_t>((size_t)std::max<int64_t>(A->nnz, 1));
   auto* ctl = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * 16));
@@ -1066,10 +1165,20 @@ void prepare(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
   P.cpos = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * ((size_t)m + 1)));
   P.values = true;
   P.sorted = true;
+  P.bspan = call.scratch_n<uint2>((size_t)std::max<int64_t>(B->nrows, 1));
+  P.arows = call.scratch_n<int64_t>((size_t)std::max<int64_t>(m, 1));
+  P.narows = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 2));
   const int sms = call.ctx()->num_sms;
+  call.before_launch("spgemm_bspan");
+  bspan_kernel<<<(unsigned)std::min<int64_t>(ceil_div(B->nrows, 256), (int64_t)sms * 8), 256, 0,
+                 call.stream()>>>(P, B->nrows);
+  call.after_launch();
   call.before_launch("spgemm_rowprod");
   rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)sms * 8), 256, 0,
                    call.stream()>>>(P);
+  call.after_launch();
+  call.before_launch("spgemm_rowprod_long");
+  rowprod_long_kernel<<<(unsigned)(sms * 8), 256, 0, call.stream()>>>(P);
   call.after_launch();
   static_assert(kNumBins + 2 <= 16, "control block");
   call.read_scalars(ctl, 16, host);
