@@ -326,6 +326,24 @@ __device__ __forceinline__ int entry_of(const int* aoff, int na, int j) {
   return lo;
 }
 
+// The same for a warp-uniform j, by the whole warp: each level samples 32
+// evenly spaced offsets in parallel and keeps the segment holding j, so a
+// row of na entries costs ceil(log32(na)) dependent loads instead of log2(na).
+__device__ __forceinline__ int entry_of_warp(const int* aoff, int na, int j) {
+  const int lane = (int)lane_id();
+  int lo = 0, hi = na;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) >> 5;
+    const int p = lo + lane * step;
+    const bool le = p < hi && aoff[p] <= j;
+    const unsigned m = __ballot_sync(kFull, le);  // lane 0 (aoff[lo] <= j) always set
+    const int L = 31 - __clz(m);
+    lo = lo + L * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
 // ---------------------------------------------------------------------------
 // tiny rows: groups of G lanes per row, one product per lane (P <= G)
 template <int G>
@@ -429,7 +447,7 @@ __device__ __forceinline__ void for_products(const SpgemmParams& P, int64_t a0, 
   if (w0 >= w1) return;
   const int* aoff = P.aoff + a0;
   // pb: A entry holding product `base`; ob: its first product (aoff[pb])
-  int pb = entry_of(aoff, na, w0);
+  int pb = entry_of_warp(aoff, na, w0);
   int ob = aoff[pb];
   const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
   for (int base = w0; base < w1; base += 32 * kBatch) {
