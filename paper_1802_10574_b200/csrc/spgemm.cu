@@ -600,14 +600,29 @@ __device__ __forceinline__ void cta_sync() {
   if constexpr (THREADS == 32) __syncwarp(); else __syncthreads();
 }
 
+// Dynamic row claims one row ahead: the claim for the next row is issued when
+// a row starts and published (by thread 0, into `sh`) when it ends, so the
+// atomic's round trip overlaps the row's work instead of preceding it.
 template <int THREADS>
-__device__ __forceinline__ int64_t claim_row(unsigned long long* claim, int64_t* sh) {
-  if (threadIdx.x == 0) *sh = (int64_t)atomicAdd(claim, 1ull);
-  cta_sync<THREADS>();
-  const int64_t r = *sh;
-  cta_sync<THREADS>();
-  return r;
-}
+struct RowClaims {
+  unsigned long long* claim;
+  int64_t* sh;
+  int64_t ahead = 0;
+  __device__ RowClaims(unsigned long long* c, int64_t* s) : claim(c), sh(s) {
+    if (threadIdx.x == 0) *sh = (int64_t)atomicAdd(claim, 1ull);
+  }
+  __device__ __forceinline__ int64_t next() {
+    cta_sync<THREADS>();
+    const int64_t r = *sh;
+    cta_sync<THREADS>();
+    if (threadIdx.x == 0) ahead = (int64_t)atomicAdd(claim, 1ull);
+    return r;
+  }
+  // before the row's last barrier
+  __device__ __forceinline__ void publish() {
+    if (threadIdx.x == 0) *sh = ahead;
+  }
+};
 
 // CTA total of one int per thread; `sh` is zero on entry and left zero for
 // the next call (the caller's next CTA barrier orders the reset).
@@ -756,9 +771,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 64 ? 2048 / THREADS : 32)
                                                                  unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   HashKeysSmem<TB>& S = *reinterpret_cast<HashKeysSmem<TB>*>(smem_raw);
-  if (threadIdx.x == 0) S.scan[0] = 0;  // cta_sum's accumulator (claim_row syncs)
+  if (threadIdx.x == 0) S.scan[0] = 0;  // cta_sum's accumulator (the claim syncs)
+  RowClaims<THREADS> rc(claim, &S.claimed);
   while (true) {
-    const int64_t r = claim_row<THREADS>(claim, &S.claimed);
+    const int64_t r = rc.next();
     if (r >= nrows) break;
     const int64_t i = rows[r];
     const int total = (int)P.prod[i];
@@ -777,6 +793,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS >= 64 ? 2048 / THREADS : 32)
     });
     const int tot = cta_sum<THREADS>(created, S.scan);
     if (threadIdx.x == 0) P.cpos[i + 1] = tot;
+    rc.publish();
     cta_sync<THREADS>();
   }
 }
@@ -788,8 +805,9 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 
                                                                 unsigned long long* claim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   HashSmem<TB>& S = *reinterpret_cast<HashSmem<TB>*>(smem_raw);
+  RowClaims<THREADS> rc(claim, &S.claimed);
   while (true) {
-    const int64_t r = claim_row<THREADS>(claim, &S.claimed);
+    const int64_t r = rc.next();
     if (r >= nrows) break;
     const int64_t i = rows[r];
     const int64_t dst = P.cpos[i];  // issued early, used by the drain
@@ -820,6 +838,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 
     // rank the runs (mutually ordered) and write the row in column order
     drain_table<THREADS>(S.keys, P.values ? S.vals : nullptr, nslots, sm.c0, P.cidx + dst,
                          P.cvals + dst, S.scan, P.sorted);
+    rc.publish();
     cta_sync<THREADS>();
   }
 }
@@ -862,8 +881,9 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
   auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
   const int nw = (int)((P.n + 63) >> 6);
   int* wpre = reinterpret_cast<int*>(bits + nw);
+  RowClaims<kLongThreads> rc(claim, &S.claimed);
   while (true) {
-    const int64_t r = claim_row<kLongThreads>(claim, &S.claimed);
+    const int64_t r = rc.next();
     if (r >= nrows) break;
     const int64_t i = rows[r];
     const int64_t dst = soff[r];
@@ -923,6 +943,7 @@ __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const Spgemm
         atomicAdd(&sval[dst + slot], v);
       });
     }
+    rc.publish();
     __syncthreads();
   }
 }
