@@ -119,6 +119,21 @@ struct SliceTracker {
 #ifndef DQ_MINB
 #define DQ_MINB 2
 #endif
+// A lane's 32-byte slice of a factor row: one 256-bit load (sm_100) when the
+// factors are 32-byte aligned, else two 128-bit loads.
+template <bool k256>
+__device__ __forceinline__ void ld_row32(const double* p, double2& a, double2& b) {
+  if constexpr (k256) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+        : "l"(p));
+  } else {
+    a = __ldg(reinterpret_cast<const double2*>(p));
+    b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  }
+}
+
+template <bool k256>
 __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const DenseParams P) {
   const int lane = (int)lane_id();
   const int q = lane >> 3;
@@ -196,9 +211,7 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
         const int j = __shfl_sync(kFull, mj, src & 31);
         double2 c0 = make_double2(0.0, 0.0), c1 = c0;
         if (fv) {
-          const double2* cr = reinterpret_cast<const double2*>(P.C + (int64_t)j * 32 + col);
-          c0 = __ldg(cr);
-          c1 = __ldg(cr + 1);
+          ld_row32<k256>(P.C + (int64_t)j * 32 + col, c0, c1);
         }
         int kk = pk;
         double bb = pb;
@@ -240,9 +253,7 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
               const bool ok = zb + uu < len;
               b[u] = ok ? bv : 0.0;
               if (ok) {
-                const double2* dr = reinterpret_cast<const double2*>(P.D + (int64_t)k * 32 + col);
-                d[u][0] = __ldg(dr);
-                d[u][1] = __ldg(dr + 1);
+                ld_row32<k256>(P.D + (int64_t)k * 32 + col, d[u][0], d[u][1]);
               } else {
                 d[u][0] = make_double2(0.0, 0.0);
                 d[u][1] = d[u][0];
@@ -923,7 +934,13 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       call.after_launch();
       call.before_launch(fast ? "mttkrp_dense32" : "mttkrp_dense_generic");
       if (fast)
-        mttkrp_dense32q_kernel<<<(unsigned)(sms * DQ_MINB), 256, 0, call.stream()>>>(P);
+      {
+        const bool a32 = ((uintptr_t)P.C % 32 == 0) && ((uintptr_t)P.D % 32 == 0);
+        if (a32)
+          mttkrp_dense32q_kernel<true><<<(unsigned)(sms * DQ_MINB), 256, 0, call.stream()>>>(P);
+        else
+          mttkrp_dense32q_kernel<false><<<(unsigned)(sms * DQ_MINB), 256, 0, call.stream()>>>(P);
+      }
       else
         mttkrp_dense_generic_kernel<<<(unsigned)(sms * 4), 256, 0, call.stream()>>>(P);
       call.after_launch();

@@ -51,6 +51,7 @@ enum Bin : int {
   kBinTiny32,
   kBinHashXS,
   kBinHashS,
+  kBinHashM1,
   kBinHashM,
   kBinHashL1,
   kBinHashL,
@@ -68,6 +69,7 @@ __host__ __device__ inline int bin_of(int64_t p) {
   if (p <= 32) return kBinTiny32;
   if (p <= 64) return kBinHashXS;
   if (p <= 256) return kBinHashS;
+  if (p <= 512) return kBinHashM1;
   if (p <= 1024) return kBinHashM;
   if (p <= 2048) return kBinHashL1;
   if (p <= 4096) return kBinHashL;
@@ -1303,6 +1305,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], false);
     launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic", claims + 0);
     launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1);
+    launch_hash<128, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], false, "spgemm_hashM1_symbolic", claims + 12);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], false, "spgemm_hashL1_symbolic", claims + 10);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
@@ -1333,6 +1336,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true);
     launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5);
     launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6);
+    launch_hash<128, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], true, "spgemm_hashM1_numeric", claims + 13);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);

@@ -20,7 +20,7 @@ cap() {  # name config scale regex skip
       timeout 300 python tools/profile_step.py --config $2 --scale $3 --steps 2 > $OUT/ncu_$1.log 2>&1
 }
 cap spadd_tiles 2 1.0 spadd_tiles 1
-cap spgemm_cfg1_hashM 1 1.0 hash_numeric 1
+cap spgemm_cfg1_hashM1 1 1.0 hash_numeric 1
 cap spgemm_cfg3_long 3 1.0 long_numeric 0
 cap spgemm_cfg3_hashM 3 1.0 hash_numeric 2
 cap mttkrp_dense32 4 1.0 mttkrp_dense32q 0

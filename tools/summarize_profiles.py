@@ -14,7 +14,7 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 WORKLOAD = {  # capture name -> (bench workload, kernel label used by the library)
     "spadd_tiles": ("spadd3_200k_50perrow", "spadd_tiles<u32>"),
-    "spgemm_cfg1_hashM": ("spgemm_10k_20perrow", "spgemm_hashM_numeric"),
+    "spgemm_cfg1_hashM1": ("spgemm_10k_20perrow", "spgemm_hashM1_numeric"),
     "spgemm_cfg3_long": ("spgemm_AxA_1M_powerlaw", "spgemm_long_numeric"),
     "spgemm_cfg3_hashM": ("spgemm_AxA_1M_powerlaw", "spgemm_hashM_numeric"),
     "mttkrp_dense32": ("mttkrp_dense_nell2shape_R32", "mttkrp_dense32"),
