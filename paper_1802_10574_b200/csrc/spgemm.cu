@@ -990,7 +990,8 @@ __global__ void __launch_bounds__(kCopyThreads) long_copy_kernel(const SpgemmPar
 // ---------------------------------------------------------------------------
 template <int THREADS, int TB>
 void launch_hash(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
-                 bool numeric, const char* name, unsigned long long* claim) {
+                 bool numeric, const char* name, unsigned long long* claim,
+                 cudaStream_t st = nullptr) {
   if (n == 0) return;
   const size_t smem = numeric ? sizeof(HashSmem<TB>) : sizeof(HashKeysSmem<TB>);
   auto kern = numeric ? hash_numeric_kernel<THREADS, TB> : hash_symbolic_kernel<THREADS, TB>;
@@ -998,9 +999,10 @@ void launch_hash(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows,
   int per_sm = 1;
   STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
   const int64_t grid = std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
-  call.before_launch(name);
-  kern<<<(unsigned)grid, THREADS, smem, call.stream()>>>(P, rows, n, claim);
-  call.after_launch();
+  if (!st) st = call.stream();
+  call.before_launch(name, st);
+  kern<<<(unsigned)grid, THREADS, smem, st>>>(P, rows, n, claim);
+  call.after_launch(st);
 }
 
 // Long rows: scratch offsets (products prefix over the long rows), the
@@ -1045,9 +1047,8 @@ LongScratch launch_long(stamrt::Call& call, const SpgemmParams& P, const int64_t
 // The copy is bandwidth-bound and the hash numeric tiers are not: it runs on
 // the auxiliary stream, overlapped with them (the caller joins before the end).
 void launch_long_copy(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
-                      const LongScratch& L) {
+                      const LongScratch& L, cudaStream_t aux) {
   if (n == 0) return;
-  cudaStream_t aux = call.fork();
   call.before_launch("spgemm_long_copy", aux);
   long_copy_kernel<<<(unsigned)std::min<int64_t>(n, (int64_t)call.ctx()->num_sms * 2), kCopyThreads,
                      0, aux>>>(P, rows, n, L.soff, L.sidx, L.sval);
@@ -1056,17 +1057,19 @@ void launch_long_copy(stamrt::Call& call, const SpgemmParams& P, const int64_t* 
 
 template <int G>
 void launch_tiny(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
-                 bool numeric) {
+                 bool numeric,
+                 cudaStream_t st = nullptr) {
   if (n == 0) return;
   const int64_t threads = n * G;
   const unsigned grid =
       (unsigned)std::min<int64_t>(stamrt::ceil_div(threads, 256), (int64_t)call.ctx()->num_sms * 16);
-  call.before_launch(numeric ? "spgemm_tiny_numeric" : "spgemm_tiny_symbolic");
+  if (!st) st = call.stream();
+  call.before_launch(numeric ? "spgemm_tiny_numeric" : "spgemm_tiny_symbolic", st);
   if (numeric)
-    tiny_numeric_kernel<G><<<grid, 256, 0, call.stream()>>>(P, rows, n);
+    tiny_numeric_kernel<G><<<grid, 256, 0, st>>>(P, rows, n);
   else
-    tiny_symbolic_kernel<G><<<grid, 256, 0, call.stream()>>>(P, rows, n);
-  call.after_launch();
+    tiny_symbolic_kernel<G><<<grid, 256, 0, st>>>(P, rows, n);
+  call.after_launch(st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1299,17 +1302,20 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     }
     auto* claims = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 16));
 
-    // symbolic
-    launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], false);
-    launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], false);
-    launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], false);
-    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic", claims + 0);
-    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1);
+    // symbolic: the small-row tiers on the auxiliary stream beside the large
+    // ones (independent rows; fills each kernel's tail)
+    cudaStream_t aux = call.fork();
+    launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], false, aux);
+    launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], false, aux);
+    launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], false, aux);
+    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic", claims + 0, aux);
+    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1, aux);
     launch_hash<128, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], false, "spgemm_hashM1_symbolic", claims + 12);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], false, "spgemm_hashL1_symbolic", claims + 10);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
     const LongScratch lsc = launch_long(call, P, rows_b[kBinLong], counts[kBinLong], claims + 4);
+    call.join();
 
     // scan counts -> row pointers
     size_t temp_bytes = 0;
@@ -1329,13 +1335,15 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     P.cvals = Cr->vals;
     if (!P.values && nnz > 0)  // ASSEMBLE: index only, values defined as zero
       STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
-    launch_long_copy(call, P, rows_b[kBinLong], counts[kBinLong], lsc);
-    // numeric (ASSEMBLE: the same passes without values)
-    launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], true);
-    launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], true);
-    launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true);
-    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5);
-    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6);
+    // numeric (ASSEMBLE: the same passes without values): the long-row copy
+    // and the small-row tiers on the auxiliary stream
+    aux = call.fork();
+    launch_long_copy(call, P, rows_b[kBinLong], counts[kBinLong], lsc, aux);
+    launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], true, aux);
+    launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], true, aux);
+    launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true, aux);
+    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5, aux);
+    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6, aux);
     launch_hash<128, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], true, "spgemm_hashM1_numeric", claims + 13);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
