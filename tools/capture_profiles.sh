@@ -22,7 +22,7 @@ cap() {  # name config scale regex skip
 cap spadd_tiles 2 1.0 spadd_tiles 1
 cap spgemm_cfg1_hashM1 1 1.0 hash_numeric 1
 cap spgemm_cfg3_long 3 1.0 long_numeric 0
-cap spgemm_cfg3_hashM 3 1.0 hash_numeric 2
+cap spgemm_cfg3_hashM 3 1.0 hash_numeric 3
 cap mttkrp_dense32 4 1.0 mttkrp_dense32q 0
 cap mttkrp_sparse 5 1.0 mttkrp_sparse 0
 ls -la $OUT
