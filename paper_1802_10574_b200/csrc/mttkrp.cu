@@ -646,7 +646,12 @@ __global__ void factor_bitmap_kernel(const int64_t* pos, const int64_t* idx, int
 
 template <int W>
 __device__ __forceinline__ void load_bm(const unsigned long long* p, unsigned long long (&b)[W]) {
-  if constexpr (W % 2 == 0) {
+  if constexpr (W == 4) {
+    // one 256-bit load per bitmap row (rows are 32-byte aligned)
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+        : "=l"(b[0]), "=l"(b[1]), "=l"(b[2]), "=l"(b[3])
+        : "l"(p));
+  } else if constexpr (W % 2 == 0) {
 #pragma unroll
     for (int k = 0; k < W; k += 2) {
       const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p) + k / 2);
