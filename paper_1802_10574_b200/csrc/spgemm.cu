@@ -855,10 +855,6 @@ struct LongHeader {
 
 __host__ __device__ inline size_t long_header() { return (sizeof(LongHeader) + 15) & ~(size_t)15; }
 
-__host__ __device__ inline size_t long_smem_bytes(int64_t n, bool numeric) {
-  const size_t nw = (size_t)((n + 63) / 64);
-  return long_header() + nw * 8 + (numeric ? nw * 4 : 0);
-}
 
 __device__ __forceinline__ void set_bit(unsigned long long* bits, int64_t col) {
   atomicOr(&bits[col >> 6], 1ull << (col & 63));
@@ -871,80 +867,100 @@ __device__ __forceinline__ void set_bit(unsigned long long* bits, int64_t col) {
 // the exact count to cpos[i+1].  After the scan long_copy_kernel moves the
 // rows into C.  (Replaces a symbolic bitmap pass + a numeric bitmap pass:
 // the products are enumerated twice instead of three times.)
+//
+// Matrices wider than the shared-memory bitmap (win_words 64-bit words,
+// ~1.2M columns) are processed in column windows of win_words * 64 columns,
+// in column order, each window enumerating the row's products again and
+// keeping those that fall inside it.
 __global__ void __launch_bounds__(kLongThreads) long_numeric_kernel(const SpgemmParams P,
                                                                     const int64_t* rows,
                                                                     int64_t nrows,
                                                                     unsigned long long* claim,
                                                                     const int64_t* soff,
                                                                     uint32_t* sidx,
-                                                                    double* sval) {
+                                                                    double* sval,
+                                                                    int win_words) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LongHeader& S = *reinterpret_cast<LongHeader*>(smem_raw);
   auto* bits = reinterpret_cast<unsigned long long*>(smem_raw + long_header());
-  const int nw = (int)((P.n + 63) >> 6);
-  int* wpre = reinterpret_cast<int*>(bits + nw);
+  const int64_t nw_all = (P.n + 63) >> 6;
+  int* wpre = reinterpret_cast<int*>(bits + win_words);
   RowClaims<kLongThreads> rc(claim, &S.claimed);
   while (true) {
     const int64_t r = rc.next();
     if (r >= nrows) break;
     const int64_t i = rows[r];
-    const int64_t dst = soff[r];
-    for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
-    __syncthreads();
     const int64_t a0 = P.apos[i];
     const int na = (int)(P.apos[i + 1] - a0);
     const int total = (int)P.prod[i];
-    for_products<false>(P, a0, na, total, [&](int64_t col, double) { set_bit(bits, col); });
-    __syncthreads();
-    // exclusive popcount prefix per word and the sorted column list: warp w
-    // owns words [w*per_w, (w+1)*per_w), lane-interleaved in 32-word chunks
-    int cnt;
-    {
-      const int lane = (int)lane_id();
-      const int warp = threadIdx.x >> 5;
-      const int per_w = (nw + 31) / 32;
-      const int ww0 = min(nw, warp * per_w), ww1 = min(nw, ww0 + per_w);
-      int mine = 0;
-      for (int w = ww0 + lane; w < ww1; w += 32) mine += __popcll(bits[w]);
-      mine = warp_sum(mine);
-      if (lane == 0) S.scan[warp] = mine;
+    int64_t dst = soff[r];
+    int64_t row_cnt = 0;
+    for (int64_t wbase = 0; wbase < nw_all; wbase += win_words) {
+      const int nw = (int)min((int64_t)win_words, nw_all - wbase);
+      const int64_t c0 = wbase * 64, c1 = (wbase + nw) * 64;  // the window's columns
+      const bool whole = wbase == 0 && nw == nw_all;
+      for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0ull;
       __syncthreads();
-      if (warp == 0) {
-        const int v = S.scan[lane];
-        const int inc = warp_inclusive_scan(v);
-        S.scan[lane] = inc - v;
-        if (lane == 31) S.scan[32] = inc;
-      }
-      __syncthreads();
-      cnt = S.scan[32];
-      int run = S.scan[warp];
-      for (int w = ww0; w < ww1; w += 32) {
-        const int wl = w + lane;
-        const unsigned long long bm = wl < ww1 ? bits[wl] : 0ull;
-        const int c = __popcll(bm);
-        const int inc = warp_inclusive_scan(c);
-        int pos = run + inc - c;
-        if (wl < ww1) wpre[wl] = pos;
-        unsigned long long mm = bm;
-        while (mm) {
-          const int b = __ffsll((long long)mm) - 1;
-          sidx[dst + pos] = (uint32_t)(wl * 64 + b);
-          pos++;
-          mm &= mm - 1;
-        }
-        run += __shfl_sync(kFull, inc, 31);
-      }
-    }
-    if (threadIdx.x == 0) P.cpos[i + 1] = cnt;
-    if (P.values) {
-      for (int t = threadIdx.x; t < cnt; t += blockDim.x) sval[dst + t] = 0.0;
-      __syncthreads();
-      for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
-        const int w = (int)(col >> 6);
-        const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
-        atomicAdd(&sval[dst + slot], v);
+      for_products<false>(P, a0, na, total, [&](int64_t col, double) {
+        if (whole || (col >= c0 && col < c1)) set_bit(bits, col - c0);
       });
+      __syncthreads();
+      // exclusive popcount prefix per word and the sorted column list: warp w
+      // owns words [w*per_w, (w+1)*per_w), lane-interleaved in 32-word chunks
+      int cnt;
+      {
+        const int lane = (int)lane_id();
+        const int warp = threadIdx.x >> 5;
+        const int per_w = (nw + 31) / 32;
+        const int ww0 = min(nw, warp * per_w), ww1 = min(nw, ww0 + per_w);
+        int mine = 0;
+        for (int w = ww0 + lane; w < ww1; w += 32) mine += __popcll(bits[w]);
+        mine = warp_sum(mine);
+        if (lane == 0) S.scan[warp] = mine;
+        __syncthreads();
+        if (warp == 0) {
+          const int v = S.scan[lane];
+          const int inc = warp_inclusive_scan(v);
+          S.scan[lane] = inc - v;
+          if (lane == 31) S.scan[32] = inc;
+        }
+        __syncthreads();
+        cnt = S.scan[32];
+        int run = S.scan[warp];
+        for (int w = ww0; w < ww1; w += 32) {
+          const int wl = w + lane;
+          const unsigned long long bm = wl < ww1 ? bits[wl] : 0ull;
+          const int c = __popcll(bm);
+          const int inc = warp_inclusive_scan(c);
+          int pos = run + inc - c;
+          if (wl < ww1) wpre[wl] = pos;
+          unsigned long long mm = bm;
+          while (mm) {
+            const int b = __ffsll((long long)mm) - 1;
+            sidx[dst + pos] = (uint32_t)(c0 + (int64_t)wl * 64 + b);
+            pos++;
+            mm &= mm - 1;
+          }
+          run += __shfl_sync(kFull, inc, 31);
+        }
+      }
+      if (P.values) {
+        for (int t = threadIdx.x; t < cnt; t += blockDim.x) sval[dst + t] = 0.0;
+        __syncthreads();
+        for_products<true>(P, a0, na, total, [&](int64_t col, double v) {
+          if (whole || (col >= c0 && col < c1)) {
+            const int64_t cc = col - c0;
+            const int w = (int)(cc >> 6);
+            const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (cc & 63)) - 1ull));
+            atomicAdd(&sval[dst + slot], v);
+          }
+        });
+      }
+      dst += cnt;
+      row_cnt += cnt;
+      __syncthreads();  // the window's bitmap and prefix are reused
     }
+    if (threadIdx.x == 0) P.cpos[i + 1] = row_cnt;
     rc.publish();
     __syncthreads();
   }
@@ -1033,13 +1049,18 @@ LongScratch launch_long(stamrt::Call& call, const SpgemmParams& P, const int64_t
   const int64_t tot = call.read_scalar(L.soff + n);
   L.sidx = call.scratch_n<uint32_t>((size_t)std::max<int64_t>(tot, 1));
   if (P.values) L.sval = call.scratch_n<double>((size_t)std::max<int64_t>(tot, 1));
-  const size_t smem = long_smem_bytes(P.n, true);
+  // bitmap + word prefix of one column window in shared memory (12 bytes per
+  // 64 columns): the whole row when B is narrow enough, else windows
+  const int64_t nw_all = (P.n + 63) / 64;
+  const int64_t max_words = ((int64_t)call.ctx()->smem_optin - (int64_t)long_header()) / 12 / 32 * 32;
+  const int win_words = (int)std::min<int64_t>(nw_all, max_words);
+  const size_t smem = long_header() + (size_t)win_words * 12;
   STAM_CUDA_CHECK(cudaFuncSetAttribute(long_numeric_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = std::min<int64_t>(n, call.ctx()->num_sms);
   call.before_launch("spgemm_long_numeric");
-  long_numeric_kernel<<<(unsigned)grid, kLongThreads, smem, call.stream()>>>(P, rows, n, claim,
-                                                                             L.soff, L.sidx, L.sval);
+  long_numeric_kernel<<<(unsigned)grid, kLongThreads, smem, call.stream()>>>(
+      P, rows, n, claim, L.soff, L.sidx, L.sval, win_words);
   call.after_launch();
   return L;
 }
@@ -1270,10 +1291,6 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     P.values = call.opts().mode == STAM_MODE_FUSED;
     P.sorted = call.opts().sort != 0;
     const int64_t products = host[kNumBins];
-    if (host[kBinLong] > 0 && long_smem_bytes(n, true) > call.ctx()->smem_optin)
-      fail(STAM_ERR_UNSUPPORTED_MERGE,
-           "spgemm: rows with more than 4096 products need a column bitmap of B's columns in "
-           "shared memory (at most ~1.2M columns in ABI v1)");
     unsigned long long counts[kNumBins], offsets[kNumBins];
     bin_rows(call, P, host, counts, offsets);
 

@@ -126,3 +126,20 @@ def test_spgemm_counters(ctx):
     expect = int(np.sum(np.diff(B.pos)[A.idx]))
     assert st.mults == expect
     assert st.appends == ctx.spgemm(_d(A), _d(B)).nnz
+
+
+def test_spgemm_wide_long_rows_column_windows(ctx):
+    # B has 3M columns (wider than a shared-memory bitmap): rows with more than
+    # 4096 products take the long-row path in column windows
+    rng = np.random.default_rng(21)
+    n, used, per_b, m, per_a = 3_000_000, 1000, 100, 48, 80
+    blens = np.zeros(n, dtype=np.int64)
+    blens[:used] = per_b
+    bpos = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(blens, out=bpos[1:])
+    B = G.csr_from_lengths(n, n, bpos, 22)
+    aidx = np.concatenate([np.sort(rng.choice(used, per_a, replace=False)) for _ in range(m)])
+    A = CSR(m, n, np.arange(m + 1, dtype=np.int64) * per_a, aidx.astype(np.int64),
+            rng.uniform(-1, 1, m * per_a))
+    C = ctx.spgemm(_d(A), _d(B))
+    oracle.compare_csr(C, oracle.spgemm(A, B, nthreads=oracle.threads_default()))
