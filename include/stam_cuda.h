@@ -216,7 +216,9 @@ STAM_CUDA_API int stam_cuda_spgemm_compute(stam_cuda_ctx* ctx, const stam_csr_vi
  * workspace in operand order, no pairwise merge:
  *   forall(i) ((forall(j) D(i,j) = w0(j)) where ((forall(j) w0(j) = B(i,j) ;
  *                forall(j) w0(j) += C(i,j) ; ...)))   (test_transform.cpp:275-284)
- * nops >= 2, all operands of equal dimensions. */
+ * nops >= 2, all operands of equal dimensions; any count (beyond 16 the
+ * workspace sequence continues across kernel calls with the partial sum as
+ * operand 0 — bit-identical to one pass). */
 STAM_CUDA_API int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops,
                                   const stam_csr_view* ops,
                                   const stam_options* opts, stam_csr_result* D,

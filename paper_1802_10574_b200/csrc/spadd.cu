@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -868,15 +869,16 @@ __global__ void spadd_compute_rows_kernel(const SpaddParams P, const int64_t* ip
 
 using namespace stamrt;
 
-extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,
-                               const stam_options* opts, stam_csr_result* D, stam_stats* stats) {
+namespace {
+int spadd_call(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,
+               const stam_options* opts, stam_csr_result* D, stam_stats* stats) {
   using namespace stamgpu;
   return guarded([&] {
     Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
     if (!ops) fail(STAM_ERR_PRECONDITION_VIOLATED, "null operand array");
     if (nops < 2) fail(STAM_ERR_ARITY_MISMATCH, "spadd needs at least two operands");
     if (nops > kMaxOps)
-      fail(STAM_ERR_UNSUPPORTED_MERGE, "spadd supports at most 16 operands per call");
+      fail(STAM_ERR_UNSUPPORTED_MERGE, "spadd supports at most 16 operands per kernel call");
     for (int p = 0; p < nops; p++) {
       check_csr_view(&ops[p], "spadd operand");
       if (ops[p].nrows != ops[0].nrows || ops[p].ncols != ops[0].ncols)
@@ -1071,6 +1073,62 @@ extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_
     st->ws_resets = nrows;
     st->appends = nnz;
   });
+}
+
+}  // namespace
+
+// More than kMaxOps operands: the workspace sequence continued across calls.
+// The partial sum of the first 16 operands is operand 0 of the next call
+// (assigned — the value the workspace holds at that point), the next 15
+// operands accumulate, and so on; a column first seen in a later operand
+// accumulates into 0.0 either way, so the result is bit-identical to one
+// workspace pass over all operands in order.  Partial sums stay on the device.
+extern "C" int stam_cuda_spadd(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,
+                               const stam_options* opts, stam_csr_result* D, stam_stats* stats) {
+  using namespace stamgpu;
+  if (nops <= kMaxOps || !ops) return spadd_call(ctx, nops, ops, opts, D, stats);
+  stam_options o = opts ? *opts : stam_options{1, STAM_MODE_FUSED, STAM_MEM_DEVICE, 0};
+  stam_options mid = o;
+  mid.result_mem = STAM_MEM_DEVICE;
+  stam_stats total{}, part{};
+  stam_csr_result acc{};
+  int st = spadd_call(ctx, kMaxOps, ops, &mid, &acc, &part);
+  // counters of one workspace pass: the partial sum re-entering as operand 0
+  // is not a new insert, and the rows are reset once
+  auto add_stats = [&](int64_t reentered) {
+    total.adds += part.adds;
+    total.ws_inserts += part.ws_inserts - reentered;
+    total.ws_resets = part.ws_resets;
+    total.appends = part.appends;
+    total.kernel_launches += part.kernel_launches;
+    total.total_kernel_ms += part.total_kernel_ms;
+    if (part.main_kernel_ms > total.main_kernel_ms) {
+      total.main_kernel_ms = part.main_kernel_ms;
+      std::memcpy(total.main_kernel, part.main_kernel, sizeof(total.main_kernel));
+    }
+  };
+  if (st != 0) return st;
+  add_stats(0);
+  int32_t next = kMaxOps;
+  while (st == 0) {
+    const int32_t take = std::min<int32_t>(kMaxOps - 1, nops - next);
+    const bool last = next + take == nops;
+    std::vector<stam_csr_view> v((size_t)take + 1);
+    v[0] = stam_csr_view{acc.nrows, acc.ncols, acc.nnz, acc.pos, acc.idx, acc.vals, acc.mem, 0};
+    for (int32_t q = 0; q < take; q++) v[(size_t)q + 1] = ops[next + q];
+    stam_csr_result out{};
+    part = stam_stats{};
+    const int64_t reentered = acc.nnz;
+    st = spadd_call(ctx, take + 1, v.data(), last ? &o : &mid, last ? D : &out, &part);
+    stam_cuda_release(ctx, acc.handle);
+    if (st != 0) break;
+    add_stats(reentered);
+    next += take;
+    if (last) break;
+    acc = out;
+  }
+  if (st == 0 && stats) *stats = total;
+  return st;
 }
 
 extern "C" int stam_cuda_spadd_compute(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,

@@ -135,3 +135,18 @@ def test_spadd_mid_rows_take_the_cta_path(ctx):
     # assemble mode through the same path
     Dz = ctx.spadd(_dev(ops), mode="assemble")
     assert np.array_equal(Dz.idx.cpu().numpy(), D.idx.cpu().numpy())
+
+
+@pytest.mark.parametrize("k", [17, 33])
+def test_spadd_more_operands_than_one_kernel_call(ctx, k):
+    # > 16 operands: the workspace sequence continues across kernel calls with
+    # the partial sum as operand 0 — bit-identical to one pass in order
+    rng = np.random.default_rng(k)
+    ops = []
+    for q in range(k):
+        lens = rng.integers(0, 12, size=300)
+        pos = np.zeros(301, dtype=np.int64)
+        np.cumsum(lens, out=pos[1:])
+        ops.append(G.csr_from_lengths(300, 400, pos, 500 + q))
+    D = ctx.spadd(_dev(ops), result="host")
+    oracle.compare_csr(D, oracle.spadd(ops), exact_values=True)
