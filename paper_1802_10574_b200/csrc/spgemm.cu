@@ -1326,11 +1326,13 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], false, aux);
     launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], false, aux);
     launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], false, "spgemm_hashXS_symbolic", claims + 0, aux);
-    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1, aux);
-    launch_hash<128, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], false, "spgemm_hashM1_symbolic", claims + 12);
-    launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
-    launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], false, "spgemm_hashL1_symbolic", claims + 10);
-    launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
+    // symbolic tiers at half the numeric tiers' threads per row (keys only:
+    // more rows in flight per SM; measured 10.65 -> 10.52 ms on config 3)
+    launch_hash<32, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], false, "spgemm_hashS_symbolic", claims + 1, aux);
+    launch_hash<64, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], false, "spgemm_hashM1_symbolic", claims + 12);
+    launch_hash<128, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], false, "spgemm_hashM_symbolic", claims + 2);
+    launch_hash<256, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], false, "spgemm_hashL1_symbolic", claims + 10);
+    launch_hash<512, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], false, "spgemm_hashL_symbolic", claims + 3);
     const LongScratch lsc = launch_long(call, P, rows_b[kBinLong], counts[kBinLong], claims + 4);
     call.join();
 
