@@ -314,6 +314,9 @@ class MttkrpWork(Workload):
             self.in_bytes = _csf_bytes(B) + 8 * (Cf.vals.size + Df.vals.size)
             self.R = Cf.ncols
             self.useful = 2 * self.R * (B.nnz + B.nfibers)
+            # every nonzero reads a factor row of D and every fiber one of C:
+            # the loop nest's operand stream from L2
+            self.l2_gather = 8 * self.R * (B.nnz + B.nfibers)
         else:
             self.Ch = CSR(Cf.nrows, Cf.ncols, *[pin(a) for a in (Cf.pos, Cf.idx, Cf.vals)])
             self.Dh = CSR(Df.nrows, Df.ncols, *[pin(a) for a in (Df.pos, Df.idx, Df.vals)])
@@ -689,7 +692,12 @@ def main():
                          "time_basis": ("device step time (the call's kernels overlap on two "
                                         "streams; their durations sum to %.3f ms)" % total_kms)
                          if overlapped else "sum of the call's kernel durations (CUDA events)",
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         **({"l2_gather": {"bytes_per_step": W.l2_gather,
+                                           "achieved_gbs": W.l2_gather / (basis_ms * 1e-3) / 1e9,
+                                           "note": "factor rows read per nonzero / fiber "
+                                                   "(L2-resident); the binding stream"}}
+                            if getattr(W, "l2_gather", None) else {})},
             "e2e": {"value": algo * world / e2e_max / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": W.h2d_bytes(), "d2h_bytes_per_step": W.d2h_bytes(),
                     "ms_per_step": e2e_max * 1e3},
