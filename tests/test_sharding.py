@@ -88,3 +88,84 @@ def test_distributed_spgemm_gloo_world2():
     res = dict(q.get(timeout=5) for _ in range(2))
     assert res.get("ok") == 0, res
     assert res.get("rank1", 0) > 0  # rank 1 owns a later row block
+
+
+def _worker_more(rank, world, port, q):
+    """SpAdd, dense MTTKRP (fiber-balanced, heavy slice cut between ranks) and
+    sparse MTTKRP (slice-aligned) through the N>1 orchestration on gloo."""
+    import torch.distributed as dist
+
+    import oracle
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    try:
+        def as_csr(o):
+            return CSR(o["nrows"], o["ncols"], o["pos"], o["idx"], o["vals"])
+
+        c2 = G.make_config(2, scale=0.002) if rank == 0 else None
+        _, D = S.distributed_spadd(c2["ops"] if c2 else None, lambda ops: as_csr(oracle.spadd(ops)),
+                                   gather=True)
+        c4 = G.make_config(4, scale=0.003) if rank == 0 else None
+        A4 = S.distributed_mttkrp_dense(
+            c4["B"] if c4 else None, c4["C"].vals if c4 else None, c4["D"].vals if c4 else None,
+            lambda b, c, d: oracle.mttkrp_dense(b, c, d)["vals"] if b.dims[0] else
+            np.zeros((0, c.shape[1])))
+        c5 = G.make_config(5, scale=0.0005) if rank == 0 else None
+        _, A5 = S.distributed_mttkrp_sparse(c5["B"] if c5 else None, c5["C"] if c5 else None,
+                                            c5["D"] if c5 else None,
+                                            lambda b, c, d: as_csr(oracle.mttkrp_sparse(b, c, d)),
+                                            gather=True)
+        if rank == 0:
+            r2 = oracle.spadd(c2["ops"])
+            out["spadd"] = bool(np.array_equal(D.pos, r2["pos"]) and np.array_equal(D.idx, r2["idx"])
+                                and np.array_equal(D.vals.view(np.int64), r2["vals"].view(np.int64)))
+            r4 = oracle.mttkrp_dense(c4["B"], c4["C"].vals, c4["D"].vals)
+            bound = 1e-12 * np.maximum(np.abs(r4["vals"]), r4["abs"])
+            out["mttkrp_dense"] = bool(np.all(np.abs(A4 - r4["vals"]) <= bound))
+            # the fiber split really cuts a slice between the ranks
+            fb = S.fiber_bounds(c4["B"], world)
+            pos1 = np.asarray(c4["B"].pos1)
+            out["cut_inside_slice"] = bool(not np.isin(fb[1:-1], pos1).all())
+            r5 = oracle.mttkrp_sparse(c5["B"], c5["C"], c5["D"])
+            out["mttkrp_sparse"] = bool(np.array_equal(A5.pos, r5["pos"]) and
+                                        np.array_equal(A5.idx, r5["idx"]) and
+                                        np.array_equal(A5.vals.view(np.int64),
+                                                       r5["vals"].view(np.int64)))
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_spadd_and_mttkrp_gloo_world2():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_more, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = q.get(timeout=5)
+    assert res == {"spadd": True, "mttkrp_dense": True, "cut_inside_slice": True,
+                   "mttkrp_sparse": True}, res
+
+
+def test_csf_fibers_partial_slices_sum_to_the_whole():
+    import oracle
+
+    cfg = G.make_config(4, scale=0.003)
+    B, Cv, Dv = cfg["B"], cfg["C"].vals, cfg["D"].vals
+    ref = oracle.mttkrp_dense(B, Cv, Dv)
+    for parts in (2, 3, 7):
+        fb = S.fiber_bounds(B, parts)
+        A = np.zeros_like(ref["vals"])
+        for p in range(parts):
+            s0, sub = S.csf_fibers(B, int(fb[p]), int(fb[p + 1]))
+            sub.validate()
+            if sub.dims[0]:
+                A[s0:s0 + sub.dims[0]] += oracle.mttkrp_dense(sub, Cv, Dv)["vals"]
+        assert np.all(np.abs(A - ref["vals"]) <= 1e-12 * np.maximum(np.abs(ref["vals"]), ref["abs"]))
