@@ -133,6 +133,11 @@ __device__ __forceinline__ void ld_row32(const double* p, double2& a, double2& b
   }
 }
 
+#ifndef DQ_LONG_FIBER
+#define DQ_LONG_FIBER 96
+#endif
+constexpr int kLongFiber = DQ_LONG_FIBER;  // a fiber this long takes a whole warp step
+
 template <bool k256>
 __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const DenseParams P) {
   const int lane = (int)lane_id();
@@ -191,50 +196,69 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
         mz = P.pos2[fg + lane];
         mlen = (int)(P.pos2[fg + lane + 1] - mz);
       }
-      // first batch (8 nonzeros per quarter) of step 0, then one step ahead
-      int pk = 0;
-      double pb = 0.0;
-      {
-        const int64_t z0n = __shfl_sync(kFull, mz, q);
-        const int lenn = __shfl_sync(kFull, mlen, q);
-        if (q < nf && (lane & 7) < lenn) {
-          pk = (int)P.idx2[z0n + (lane & 7)];
-          pb = P.vals[z0n + (lane & 7)];
+      // Steps: up to 4 consecutive short fibers, a quarter each; or one long
+      // fiber (>= kLongFiber nonzeros) split over all four quarters (batch t
+      // covers its nonzeros [32t, 32t+32), quarter q the 8 at 32t+8q), so no
+      // quarter idles while another finishes a long fiber.
+      const unsigned longm = __ballot_sync(kFull, lane < nf && mlen >= kLongFiber);
+      auto step_at = [&](int g, bool& lmode, int& nsh) {
+        lmode = (longm >> g) & 1u;
+        const unsigned after = longm >> g;  // bit 0 = fiber g
+        const int next_long = after ? __ffs(after) - 1 : 32;
+        nsh = lmode ? 1 : min(4, min(nf - g, next_long));
+      };
+      // lane (q, l) of a step's first batch: short -> nonzero l of fiber g+q;
+      // long -> nonzero 8q+l of fiber g
+      auto first_batch = [&](int g, bool lmode, int nsh, int& k, double& b) {
+        const int src = lmode ? g : g + q;
+        const int64_t z0n = __shfl_sync(kFull, mz, src & 31);
+        const int lenn = __shfl_sync(kFull, mlen, src & 31);
+        const int zl = (lmode ? 8 * q : 0) + (lane & 7);
+        k = 0;
+        b = 0.0;
+        if ((lmode || q < nsh) && zl < lenn) {
+          k = (int)P.idx2[z0n + zl];
+          b = P.vals[z0n + zl];
         }
-      }
-      for (int g = 0; g < nf; g += 4) {
-        const int src = g + q;
-        const bool fv = src < nf;
+      };
+      bool lmode;
+      int nsh;
+      step_at(0, lmode, nsh);
+      int pk;
+      double pb;
+      first_batch(0, lmode, nsh, pk, pb);
+      for (int g = 0; g < nf;) {
+        const int src = lmode ? g : g + q;
+        const bool fv = lmode || q < nsh;
         const int64_t z0 = __shfl_sync(kFull, mz, src & 31);
         const int len_s = __shfl_sync(kFull, mlen, src & 31);  // every lane shuffles
         const int len = fv ? len_s : 0;
         const int j = __shfl_sync(kFull, mj, src & 31);
+        const int zoff = lmode ? 8 * q : 0;
+        const int stride = lmode ? 32 : 8;
         double2 c0 = make_double2(0.0, 0.0), c1 = c0;
-        if (fv) {
+        if (fv && (!lmode || q == 0)) {
           ld_row32<k256>(P.C + (int64_t)j * 32 + col, c0, c1);
         }
         int kk = pk;
         double bb = pb;
-        if (g + 4 < nf) {  // uniform: prefetch the next step's first batch
-          const int src2 = g + 4 + q;
-          const int64_t z0n = __shfl_sync(kFull, mz, src2 & 31);
-          const int lenn = __shfl_sync(kFull, mlen, src2 & 31);
-          pk = 0;
-          pb = 0.0;
-          if (src2 < nf && (lane & 7) < lenn) {
-            pk = (int)P.idx2[z0n + (lane & 7)];
-            pb = P.vals[z0n + (lane & 7)];
-          }
+        // the next step and its first batch, loaded before this one is consumed
+        const int gn = g + nsh;
+        bool lmode_n = false;
+        int nsh_n = 0;
+        if (gn < nf) {  // uniform
+          step_at(gn, lmode_n, nsh_n);
+          first_batch(gn, lmode_n, nsh_n, pk, pb);
         }
         const int nmax = __reduce_max_sync(kFull, (unsigned)len);
         double w[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int zb = 0; zb < nmax; zb += 8) {
-          // lane (q, l) holds nonzero zb + l of its quarter's fiber; load the
-          // next batch before consuming this one
+        for (int zb = 0; zb < nmax; zb += stride) {
+          // lane (q, l) holds nonzero zb + zoff + l of its quarter's stream;
+          // load the next batch before consuming this one
           int kn = 0;
           double bn = 0.0;
-          if (zb + 8 < nmax) {
-            const int zl = zb + 8 + (lane & 7);
+          if (zb + stride < nmax) {
+            const int zl = zb + stride + zoff + (lane & 7);
             if (zl < len) {
               kn = (int)P.idx2[z0 + zl];
               bn = P.vals[z0 + zl];
@@ -242,7 +266,7 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
           }
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            if (zb + 4 * h >= nmax) break;  // uniform
+            if (__all_sync(kFull, zb + zoff + 4 * h >= len)) break;  // no quarter has entries left
             double2 d[4][2];
             double b[4];
 #pragma unroll
@@ -250,7 +274,7 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
               const int uu = 4 * h + u;
               const int k = __shfl_sync(kFull, kk, qbase + uu);
               const double bv = __shfl_sync(kFull, bb, qbase + uu);
-              const bool ok = zb + uu < len;
+              const bool ok = zb + zoff + uu < len;
               b[u] = ok ? bv : 0.0;
               if (ok) {
                 ld_row32<k256>(P.D + (int64_t)k * 32 + col, d[u][0], d[u][1]);
@@ -270,10 +294,17 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
           kk = kn;
           bb = bn;
         }
-        // fibers g..g+3 in order: add the owner quarter's share, flush at slice ends
+        if (lmode) {  // the four quarters' partial sums of the one fiber (fixed order)
+#pragma unroll
+          for (int x = 0; x < 4; x++) {
+            w[x] += __shfl_xor_sync(kFull, w[x], 8);
+            w[x] += __shfl_xor_sync(kFull, w[x], 16);
+          }
+        }
+        // fibers g..g+nsh-1 in order: add the owner quarter's share, flush at slice ends
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-          if (g + u >= nf) break;  // uniform
+          if (u >= nsh) break;  // uniform
           const int64_t f = fg + g + u;
           while (f >= st.s_end) {
             st.s++;
@@ -288,6 +319,9 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
           }
           if (f + 1 == st.s_end) flush(true);
         }
+        g = gn;
+        lmode = lmode_n;
+        nsh = nsh_n;
       }
     }
     if (fb < st.s_end) flush(false);
