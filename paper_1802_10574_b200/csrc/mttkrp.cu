@@ -540,7 +540,6 @@ __global__ void mttkrp_dense_fixup_kernel(const DenseParams P, const FixupLevels
 // sparse
 // ===========================================================================
 constexpr int kSpWarps = 8;
-constexpr int kSpSlicesPerWarp = 2;  // slices per warp-level tile
 constexpr int kRowChunk = 8;         // factor-row entries held in registers at once
 
 struct SparseParams {

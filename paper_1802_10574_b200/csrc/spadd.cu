@@ -92,7 +92,6 @@ struct SpaddParams {
 
 template <typename ColT, int STAGE>
 struct WarpStage {
-  static constexpr int kStage = STAGE;
   ColT in_col[STAGE];
   ColT st_col[STAGE];
   double st_val[STAGE];
@@ -492,7 +491,6 @@ __device__ int64_t count_row_global(const SpaddParams& P, const SM& S, int r) {
 
 template <typename ColT, typename Cfg, int NOPS>
 __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
-  constexpr int kWarps = Cfg::kWarps;
   constexpr int kRowsPerWarp = Cfg::kRowsPerWarp;
   constexpr int kTileRowsC = Cfg::kTileRows;
   constexpr int kStage = Cfg::kStage;
