@@ -1063,7 +1063,9 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     const int64_t words = (R + 63) / 64;
     const int W = words <= 1 ? 1 : words <= 2 ? 2 : words <= 4 ? 4 : words <= 8 ? 8 : 0;
     auto build_bm = [&](const int64_t* pos, const int64_t* idx, int64_t nrows) {
-      auto* bm = call.scratch_n<unsigned long long>((size_t)(nrows * W));
+      // rows are read with 256-bit loads (W = 4): align the array to 32 bytes
+      auto* raw = call.scratch_n<unsigned long long>((size_t)(nrows * W) + 4);
+      auto* bm = reinterpret_cast<unsigned long long*>(((uintptr_t)raw + 31) & ~(uintptr_t)31);
       const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nrows, 256),
                                                         (int64_t)call.ctx()->num_sms * 8);
       call.before_launch("mttkrp_factor_bitmap");
