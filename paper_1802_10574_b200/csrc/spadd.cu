@@ -364,7 +364,8 @@ __device__ __forceinline__ void load_cols_padded(const SpaddParams& P, WarpStage
 }
 
 template <int NOPS, int DLOG, typename ColT, int STAGE>
-__device__ __forceinline__ int merge_flat(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L) {
+__device__ __forceinline__ int merge_flat(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
+                                          int out) {
   constexpr int D = 1 << DLOG;
   const unsigned lane = lane_id();
   int co[NOPS];
@@ -403,17 +404,18 @@ __device__ __forceinline__ int merge_flat(const SpaddParams& P, WarpStage<ColT, 
       dup |= upper && r > 0 && sq[r - 1] == x;
       m += r;
     }
-    W.st_col[m] = x;
-    W.st_val[m] = v;
-    W.st_op[m] = (uint8_t)o;
+    W.st_col[out + m] = x;
+    W.st_val[out + m] = v;
+    W.st_op[out + m] = (uint8_t)o;
   }
-  return combine_staged(W, L, 0, __any_sync(kFull, dup));
+  return combine_staged(W, L, out, __any_sync(kFull, dup));
 }
 
 // Stages and merges the row through the padded path when NOPS * D fits the
 // staging; returns -1 (nothing staged) otherwise.
 template <int NOPS, typename ColT, int STAGE>
-__device__ __forceinline__ int merge_row_padded(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L) {
+__device__ __forceinline__ int merge_row_padded(const SpaddParams& P, WarpStage<ColT, STAGE>& W, int L,
+                                                int out) {
   if constexpr (NOPS == 2 || NOPS == 3) {
     int maxlen = 0;
 #pragma unroll
@@ -422,15 +424,15 @@ __device__ __forceinline__ int merge_row_padded(const SpaddParams& P, WarpStage<
     if (dlog > 8 || (NOPS << dlog) > STAGE) return -1;
     load_cols_padded<NOPS>(P, W, 1 << dlog);
     switch (dlog) {
-      case 0: return merge_flat<NOPS, 0>(P, W, L);
-      case 1: return merge_flat<NOPS, 1>(P, W, L);
-      case 2: return merge_flat<NOPS, 2>(P, W, L);
-      case 3: return merge_flat<NOPS, 3>(P, W, L);
-      case 4: return merge_flat<NOPS, 4>(P, W, L);
-      case 5: return merge_flat<NOPS, 5>(P, W, L);
-      case 6: return merge_flat<NOPS, 6>(P, W, L);
-      case 7: return merge_flat<NOPS, 7>(P, W, L);
-      default: return merge_flat<NOPS, 8>(P, W, L);
+      case 0: return merge_flat<NOPS, 0>(P, W, L, out);
+      case 1: return merge_flat<NOPS, 1>(P, W, L, out);
+      case 2: return merge_flat<NOPS, 2>(P, W, L, out);
+      case 3: return merge_flat<NOPS, 3>(P, W, L, out);
+      case 4: return merge_flat<NOPS, 4>(P, W, L, out);
+      case 5: return merge_flat<NOPS, 5>(P, W, L, out);
+      case 6: return merge_flat<NOPS, 6>(P, W, L, out);
+      case 7: return merge_flat<NOPS, 7>(P, W, L, out);
+      default: return merge_flat<NOPS, 8>(P, W, L, out);
     }
   }
   return -1;
@@ -523,7 +525,7 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     int64_t cnt;
     int state;
     int padded = -1;
-    if (stage_off == 0 && tot <= kStage) padded = merge_row_padded<NOPS>(P, W, (int)tot);
+    if (tot <= kStage - stage_off) padded = merge_row_padded<NOPS>(P, W, (int)tot, stage_off);
     if (padded >= 0) {
       cnt = padded;
       state = kStaged;
