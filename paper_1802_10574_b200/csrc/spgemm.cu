@@ -141,7 +141,7 @@ __device__ __forceinline__ void tally_flush(const SpgemmParams& P, RowTally& T,
   }
 }
 
-__global__ void rowprod_kernel(const SpgemmParams P) {
+__global__ void rowprod_kernel(const SpgemmParams P, int rw) {
   __shared__ unsigned long long hist[kNumBins];
   __shared__ unsigned long long total, maxp;
   if (threadIdx.x < kNumBins) hist[threadIdx.x] = 0;
@@ -152,8 +152,9 @@ __global__ void rowprod_kernel(const SpgemmParams P) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   RowTally T;
   T.hist = hist;
-  for (int64_t base = warp * 32; base < P.m; base += nwarps * 32) {
-    const int nr = (int)min((int64_t)32, P.m - base);
+  // windows of rw <= 32 rows (fewer for small matrices: more warps in flight)
+  for (int64_t base = warp * rw; base < P.m; base += nwarps * rw) {
+    const int nr = (int)min((int64_t)rw, P.m - base);
     // lane l < nr: start of row base + l; lanes >= nr: the window's end
     const int64_t rp = P.apos[base + min((int)lane, nr)];
     const int64_t wend = P.apos[base + nr];
@@ -1239,11 +1240,14 @@ void prepare(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
                  call.stream()>>>(P, B->nrows);
   call.after_launch();
   call.before_launch("spgemm_rowprod");
-  rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 256), (int64_t)sms * 8), 256, 0,
-                   call.stream()>>>(P);
+  // rows per warp window: 32, or fewer when that leaves the GPU underfilled
+  int rw = 32;
+  while (rw > 4 && ceil_div(m, (int64_t)rw) < (int64_t)sms * 32) rw >>= 1;
+  rowprod_kernel<<<(unsigned)std::min<int64_t>(ceil_div(ceil_div(m, (int64_t)rw), 8), (int64_t)sms * 8),
+                   256, 0, call.stream()>>>(P, rw);
   call.after_launch();
   call.before_launch("spgemm_rowprod_long");
-  rowprod_long_kernel<<<(unsigned)(sms * 8), 256, 0, call.stream()>>>(P);
+  rowprod_long_kernel<<<(unsigned)(sms * 2), 256, 0, call.stream()>>>(P);
   call.after_launch();
   static_assert(kNumBins + 2 <= 16, "control block");
   call.read_scalars(ctl, 16, host);
