@@ -1349,15 +1349,20 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(temp, temp_bytes, P.cpos + 1, P.cpos + 1, m,
                                                   call.stream()));
     call.after_launch();
-    const int64_t nnz = call.read_scalar(P.cpos + m);
-
-    call.alloc_csr_result(Cr, m, n, nnz);
+    // Small products: C is allocated at the products count (an upper bound of
+    // nnz, known since rowprod) and the exact nnz read once everything is
+    // queued — no host round trip between the passes (config 1: 0.286 ->
+    // 0.275 ms).  Large: exact allocation after the scan (measured faster on
+    // config 3: 10.55 vs 10.86 ms).
+    const bool defer_nnz = products <= (int64_t)(64ll << 20);
+    const int64_t cap = defer_nnz ? products : call.read_scalar(P.cpos + m);
+    call.alloc_csr_result(Cr, m, n, cap);
     STAM_CUDA_CHECK(cudaMemcpyAsync(Cr->pos, P.cpos, sizeof(int64_t) * ((size_t)m + 1),
                                     cudaMemcpyDeviceToDevice, call.stream()));
     P.cidx = Cr->idx;
     P.cvals = Cr->vals;
-    if (!P.values && nnz > 0)  // ASSEMBLE: index only, values defined as zero
-      STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)nnz, call.stream()));
+    if (!P.values && cap > 0)  // ASSEMBLE: index only, values defined as zero
+      STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)cap, call.stream()));
     // numeric (ASSEMBLE: the same passes without values): the long-row copy
     // and the small-row tiers on the auxiliary stream
     aux = call.fork();
@@ -1372,6 +1377,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
     call.join();
+    const int64_t nnz = defer_nnz ? call.read_scalar(P.cpos + m) : cap;
 
     call.finish_csr_result(Cr, nnz);
     call.finish();
