@@ -959,7 +959,13 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
     // ~16 chunks per resident warp: small enough to balance the skewed
     // slices, large enough to amortize a chunk's bookkeeping
     const int64_t warps = (int64_t)sms * 32;
-    P.chunk_nnz = std::max<int64_t>(512, ceil_div(std::max<int64_t>(B->nnz, 1), warps * 16));
+#ifndef DQ_CHUNKS_PER_WARP
+#define DQ_CHUNKS_PER_WARP 32
+#endif
+#ifndef DQ_CHUNK_MIN
+#define DQ_CHUNK_MIN 512
+#endif
+    P.chunk_nnz = std::max<int64_t>(DQ_CHUNK_MIN, ceil_div(std::max<int64_t>(B->nnz, 1), warps * DQ_CHUNKS_PER_WARP));
     P.nchunks = std::max<int64_t>(1, ceil_div(B->nnz, P.chunk_nnz));
     P.part = call.scratch_n<double>((size_t)(ncb * P.nchunks * 64));
     P.part_slice = call.scratch_n<int64_t>((size_t)(2 * P.nchunks));
