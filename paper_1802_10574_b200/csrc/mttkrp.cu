@@ -539,7 +539,10 @@ __global__ void mttkrp_dense_fixup_kernel(const DenseParams P, const FixupLevels
 // ===========================================================================
 // sparse
 // ===========================================================================
-constexpr int kSpWarps = 8;
+#ifndef SP_WARPS
+#define SP_WARPS 8
+#endif
+constexpr int kSpWarps = SP_WARPS;
 constexpr int kRowChunk = 8;         // factor-row entries held in registers at once
 
 struct SparseParams {
