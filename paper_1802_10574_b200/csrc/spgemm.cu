@@ -60,7 +60,10 @@ enum Bin : int {
 };
 constexpr int kLongThreads = 1024;
 constexpr uint32_t kEmpty = 0xffffffffu;
-constexpr int kBatch = 4;  // independent product gathers in flight per lane
+#ifndef SPGEMM_BATCH
+#define SPGEMM_BATCH 4
+#endif
+constexpr int kBatch = SPGEMM_BATCH;  // independent product gathers in flight per lane
 
 __host__ __device__ inline int bin_of(int64_t p) {
   if (p == 0) return kBinEmpty;
