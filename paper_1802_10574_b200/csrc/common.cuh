@@ -59,6 +59,7 @@ __device__ __forceinline__ T warp_inclusive_scan(T v) {
 }
 
 // Read-only streaming loads (bypass L1 allocation for data touched once).
+#ifndef STAM_STREAM_PLAIN
 __device__ __forceinline__ int64_t ldg_stream(const int64_t* p) {
   return (int64_t)__ldcs((const long long*)p);
 }
@@ -67,6 +68,12 @@ __device__ __forceinline__ void stg_stream(int64_t* p, int64_t v) {
   __stcs((long long*)p, (long long)v);
 }
 __device__ __forceinline__ void stg_stream(double* p, double v) { __stcs(p, v); }
+#else  // tuning experiment: default cache policy
+__device__ __forceinline__ int64_t ldg_stream(const int64_t* p) { return __ldg(p); }
+__device__ __forceinline__ double ldg_stream(const double* p) { return __ldg(p); }
+__device__ __forceinline__ void stg_stream(int64_t* p, int64_t v) { *p = v; }
+__device__ __forceinline__ void stg_stream(double* p, double v) { *p = v; }
+#endif
 
 // ---------------------------------------------------------------------------
 // Ordered tiles with decoupled look-back.
