@@ -48,6 +48,12 @@ struct TileCfg {
   static constexpr int kTileRows = W * RPW;
   static constexpr int kStage = STAGE;
 };
+// 1: a look-back tile per warp (no CTA barriers after the tile claim);
+// 0: one look-back tile per CTA.  Measured on config 2: 0.485 ms (per CTA)
+// vs 0.614 ms (per warp: 24x more look-back tiles lengthen the prefix chain)
+#ifndef SPADD_WARP_LOOKBACK
+#define SPADD_WARP_LOOKBACK 0
+#endif
 #ifndef SPADD_MIDTHRESH
 #define SPADD_MIDTHRESH 360
 #endif
@@ -496,6 +502,7 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
   constexpr int kRowsPerWarp = Cfg::kRowsPerWarp;
   constexpr int kTileRowsC = Cfg::kTileRows;
   constexpr int kStage = Cfg::kStage;
+  static_assert(kRowsPerWarp <= 32 && Cfg::kWarps <= 32, "warp look-back tiles");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem<ColT, Cfg>& S = *reinterpret_cast<TileSmem<ColT, Cfg>*>(smem_raw);
   const unsigned lane = lane_id();
@@ -508,6 +515,16 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
   const int64_t row0 = tile * kTileRowsC;
   const int nrows_tile = (int)min((int64_t)kTileRowsC, P.nrows - row0);
 
+#if SPADD_WARP_LOOKBACK
+  // each warp loads its own rows' operand row pointers (row bounds shared with
+  // the neighbouring warp are written by both, with the same value)
+  for (int i = lane; i < nops * (kRowsPerWarp + 1); i += 32) {
+    const int p = i / (kRowsPerWarp + 1);
+    const int r = warp * kRowsPerWarp + i % (kRowsPerWarp + 1);
+    S.tpos[p][r] = (r <= nrows_tile) ? __ldg(P.pos[p] + row0 + r) : 0;
+  }
+  __syncwarp();
+#else
   // tile-wide operand row pointers
   for (int i = threadIdx.x; i < nops * (kTileRowsC + 1); i += blockDim.x) {
     const int p = i / (kTileRowsC + 1);
@@ -515,6 +532,7 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     S.tpos[p][r] = (r <= nrows_tile) ? __ldg(P.pos[p] + row0 + r) : 0;
   }
   __syncthreads();
+#endif
 
   WarpStage<ColT, kStage>& W = S.w[warp];
   int stage_off = 0;
@@ -549,6 +567,33 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     if (state == kStaged) stage_off += (int)cnt;
     __syncwarp();
   }
+#if SPADD_WARP_LOOKBACK
+  // Every warp is its own look-back tile (warp tile = tile * kWarps + warp):
+  // no CTA barrier between a warp's merge and its writes, so a warp with a
+  // long row does not hold up the other warps of its CTA.  Warps without rows
+  // publish a zero aggregate.  Predecessors are resident or done (earlier
+  // warps of this CTA, or CTAs that claimed earlier tiles).
+  {
+    const int rw0 = warp * kRowsPerWarp;
+    const int rr = rw0 + (int)lane;
+    const bool mine = (int)lane < kRowsPerWarp && rr < nrows_tile;
+    const int64_t c = mine ? S.row_cnt[rr] : 0;
+    const int64_t inc = warp_inclusive_scan(c);
+    const int64_t agg = __shfl_sync(kFull, inc, 31);
+    const int64_t wtile = tile * Cfg::kWarps + warp;
+    const int64_t base = lookback_exclusive(P.tile_status, wtile, agg);
+    if (mine) {
+      S.row_dst[rr] = base + inc - c;
+      P.out_pos[row0 + rr + 1] = base + inc;
+    }
+    if (lane == 0) {
+      if (wtile == 0) P.out_pos[0] = 0;
+      if (wtile == P.ntiles * Cfg::kWarps - 1) *P.total_nnz = base + agg;
+      if (wtile == (P.last_tile + 1) * Cfg::kWarps - 1 && P.block_end) *P.block_end = base + agg;
+    }
+    __syncwarp();
+  }
+#else
   __syncthreads();
 
   // tile aggregate and look-back (warp 0)
@@ -568,6 +613,7 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const Spa
     }
   }
   __syncthreads();
+#endif
 
   // stream out staged rows; redo postponed rows with the (now free) staging
   for (int k = 0; k < kRowsPerWarp; k++) {
@@ -944,7 +990,7 @@ int spadd_call(stam_cuda_ctx* ctx, int32_t nops, const stam_csr_view* ops,
     P.out_vals = D->vals;
     // control block: [deferred count, total, pad, pad] + one tile counter per
     // block + tile status words
-    const size_t ctl_words = 4 + (size_t)nblocks + (size_t)P.ntiles;
+    const size_t ctl_words = 4 + (size_t)nblocks + (size_t)P.ntiles * (SPADD_WARP_LOOKBACK ? 32 : 1);
     auto* ctl = static_cast<uint64_t*>(call.scratch_zero(ctl_words * sizeof(uint64_t)));
     P.deferred_count = reinterpret_cast<unsigned long long*>(ctl);
     P.total_nnz = reinterpret_cast<int64_t*>(ctl + 1);
