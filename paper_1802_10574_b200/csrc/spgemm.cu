@@ -60,6 +60,11 @@ enum Bin : int {
 };
 constexpr int kLongThreads = 1024;
 constexpr uint32_t kEmpty = 0xffffffffu;
+// threads of the hash-M1 numeric tier (rows of 256 < P <= 512 products);
+// config 1 kernel: 64 0.163 ms, 128 0.121 ms (kept), 256 0.137 ms
+#ifndef SPGEMM_M1_NUM_THREADS
+#define SPGEMM_M1_NUM_THREADS 128
+#endif
 #ifndef SPGEMM_BATCH
 #define SPGEMM_BATCH 4
 #endif
@@ -1375,7 +1380,7 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true, aux);
     launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5, aux);
     launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6, aux);
-    launch_hash<128, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], true, "spgemm_hashM1_numeric", claims + 13);
+    launch_hash<SPGEMM_M1_NUM_THREADS, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], true, "spgemm_hashM1_numeric", claims + 13);
     launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
     launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
     launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
