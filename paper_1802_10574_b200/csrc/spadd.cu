@@ -54,6 +54,10 @@ struct TileCfg {
 #ifndef SPADD_WARP_LOOKBACK
 #define SPADD_WARP_LOOKBACK 0
 #endif
+// minimum resident CTAs per SM the register budget targets (tiles kernel)
+#ifndef SPADD_MINB
+#define SPADD_MINB 1
+#endif
 #ifndef SPADD_MIDTHRESH
 #define SPADD_MIDTHRESH 360
 #endif
@@ -498,7 +502,7 @@ __device__ int64_t count_row_global(const SpaddParams& P, const SM& S, int r) {
 }
 
 template <typename ColT, typename Cfg, int NOPS>
-__global__ void __launch_bounds__(Cfg::kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
+__global__ void __launch_bounds__(Cfg::kWarps * 32, SPADD_MINB) spadd_tiles_kernel(const SpaddParams P) {
   constexpr int kRowsPerWarp = Cfg::kRowsPerWarp;
   constexpr int kTileRowsC = Cfg::kTileRows;
   constexpr int kStage = Cfg::kStage;
