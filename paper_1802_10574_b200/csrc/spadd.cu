@@ -54,9 +54,13 @@ struct TileCfg {
 #ifndef SPADD_WARP_LOOKBACK
 #define SPADD_WARP_LOOKBACK 0
 #endif
-// minimum resident CTAs per SM the register budget targets (tiles kernel)
-#ifndef SPADD_MINB
-#define SPADD_MINB 1
+// -DSPADD_MINB=n: minimum resident CTAs per SM the tiles kernel's register
+// budget targets.  Unset by default: an explicit minimum of 1 makes ptxas use
+// 64 registers instead of 40 (config 2: 0.714 vs 0.480 ms).
+#ifdef SPADD_MINB
+#define SPADD_TILES_BOUNDS(t) __launch_bounds__(t, SPADD_MINB)
+#else
+#define SPADD_TILES_BOUNDS(t) __launch_bounds__(t)
 #endif
 #ifndef SPADD_MIDTHRESH
 #define SPADD_MIDTHRESH 360
@@ -502,7 +506,7 @@ __device__ int64_t count_row_global(const SpaddParams& P, const SM& S, int r) {
 }
 
 template <typename ColT, typename Cfg, int NOPS>
-__global__ void __launch_bounds__(Cfg::kWarps * 32, SPADD_MINB) spadd_tiles_kernel(const SpaddParams P) {
+__global__ void SPADD_TILES_BOUNDS(Cfg::kWarps * 32) spadd_tiles_kernel(const SpaddParams P) {
   constexpr int kRowsPerWarp = Cfg::kRowsPerWarp;
   constexpr int kTileRowsC = Cfg::kTileRows;
   constexpr int kStage = Cfg::kStage;
