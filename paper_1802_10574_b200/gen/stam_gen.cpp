@@ -19,12 +19,22 @@
 
 namespace {
 
+// SplitMix64 finaliser: a bijective 64-bit mix.
+inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// One SplitMix64 stream per (seed, id).  The start state is a hash of both
+// (not seed*C + id*G, which put stream id+1 one draw behind stream id on the
+// same Weyl sequence and made neighbouring rows / slices shifted copies of each
+// other), so streams of different ids start at unrelated points of the 2^64
+// cycle.
 struct Stream {
   uint64_t s;
   Stream(uint64_t seed, uint64_t id) {
-    s = seed * 0xD1342543DE82EF95ull + (id + 1) * 0x9E3779B97F4A7C15ull;
-    next();
-    next();
+    s = mix64(mix64(seed ^ 0x6A09E667F3BCC909ull) ^ mix64(id + 0x3C6EF372FE94F82Bull));
   }
   uint64_t next() {
     uint64_t z = (s += 0x9E3779B97F4A7C15ull);
@@ -119,7 +129,7 @@ GEN_API int64_t gen_powerlaw_pos(int64_t nrows, double a, double q, int64_t lmin
     cdf[(size_t)(L - lmin)] = acc;
   }
   for (auto& c : cdf) c /= acc;
-  Stream rng(seed, 0x5eed);
+  Stream rng(seed, (1ull << 62) + 0x5eed);  // disjoint from the per-row ids
   pos[0] = 0;
   for (int64_t i = 0; i < nrows; i++) {
     const double u = rng.uniform();
@@ -163,7 +173,7 @@ GEN_API int gen_uniform_slice_counts(int64_t nslices, int64_t nnz, uint64_t seed
     while (true) {
       const int64_t c = next.fetch_add(1);
       if (c >= nchunks) break;
-      Stream rng(seed, 0x100000000ull + (uint64_t)c);
+      Stream rng(seed, (1ull << 61) + (uint64_t)c);
       const int64_t e = std::min(nnz, (c + 1) * chunk);
       for (int64_t p = c * chunk; p < e; p++) h[(size_t)rng.below((uint64_t)nslices)]++;
     }
