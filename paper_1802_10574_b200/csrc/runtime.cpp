@@ -42,6 +42,36 @@ Call::~Call() {
   if (aux_open_) cudaStreamSynchronize(ctx_->aux_stream);
   for (void* p : temps_) cudaFreeAsync(p, ctx_->stream);
   if (!finished_) cudaStreamSynchronize(ctx_->stream);
+  if (!finished_ && result_slot_ && *result_slot_) {
+    // failed after allocating the result: release it here
+    auto* own = static_cast<Owned*>(*result_slot_);
+    if (own->dev) cudaFreeAsync(own->dev, ctx_->stream);
+    if (own->host_pending && !own->host) own->host = own->host_pending;
+    if (own->host) pinned_recycle(own->host, own->host_bytes);
+    delete own;
+    *result_slot_ = nullptr;
+  }
+}
+
+void Call::adopt_result(void** handle_slot) { result_slot_ = handle_slot; }
+
+void Call::pinned_recycle(void* p, size_t bytes) {
+  ctx_->pinned_free.emplace_back(p, bytes);
+  if (ctx_->pinned_free.size() > 8) {
+    cudaFreeHost(ctx_->pinned_free.front().first);
+    ctx_->pinned_free.erase(ctx_->pinned_free.begin());
+  }
+}
+
+cudaEvent_t Call::next_event() {
+  if (ctx_->event_next >= ctx_->event_pool.size()) {
+    for (int e = 0; e < 64; e++) {
+      cudaEvent_t ev;
+      STAM_CUDA_CHECK(cudaEventCreate(&ev));
+      ctx_->event_pool.push_back(ev);
+    }
+  }
+  return ctx_->event_pool[ctx_->event_next++];
 }
 
 void* Call::scratch(size_t bytes) {
@@ -64,8 +94,8 @@ const void* Call::stage(const void* p, size_t bytes, int32_t mem) {
   if (mem != STAM_MEM_HOST) fail(STAM_ERR_PRECONDITION_VIOLATED, "unknown memory kind");
   if (!p) fail(STAM_ERR_PRECONDITION_VIOLATED, "null host input array");
   if (opts_.timing && !h2d_start_) {
-    h2d_start_ = ctx_->event_pool[ctx_->event_next++];
-    h2d_stop_ = ctx_->event_pool[ctx_->event_next++];
+    h2d_start_ = next_event();
+    h2d_stop_ = next_event();
     STAM_CUDA_CHECK(cudaEventRecord(h2d_start_, ctx_->stream));
   }
   void* d = scratch(bytes);
@@ -74,16 +104,7 @@ const void* Call::stage(const void* p, size_t bytes, int32_t mem) {
   return d;
 }
 
-cudaEvent_t Call::event() {
-  if (ctx_->event_next + 1 > ctx_->event_pool.size()) {
-    for (int e = 0; e < 64; e++) {
-      cudaEvent_t ev;
-      STAM_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      ctx_->event_pool.push_back(ev);
-    }
-  }
-  return ctx_->event_pool[ctx_->event_next++];
-}
+cudaEvent_t Call::event() { return next_event(); }
 
 void Call::copy_range(void* dst, const void* src, size_t bytes) {
   if (!ctx_->copy_stream)
@@ -128,15 +149,9 @@ void Call::wait(cudaEvent_t ev) { STAM_CUDA_CHECK(cudaStreamWaitEvent(ctx_->stre
 void Call::before_launch(const char* name, cudaStream_t st) {
   stats_->kernel_launches++;
   if (!opts_.timing) return;
-  if (ctx_->event_next + 2 > ctx_->event_pool.size()) {
-    for (int e = 0; e < 64; e++) {
-      cudaEvent_t ev;
-      STAM_CUDA_CHECK(cudaEventCreate(&ev));
-      ctx_->event_pool.push_back(ev);
-    }
-  }
-  TimedLaunch t{name, ctx_->event_pool[ctx_->event_next], ctx_->event_pool[ctx_->event_next + 1]};
-  ctx_->event_next += 2;
+  TimedLaunch t{name, nullptr, nullptr};
+  t.start = next_event();
+  t.stop = next_event();
   STAM_CUDA_CHECK(cudaEventRecord(t.start, st ? st : ctx_->stream));
   launches_.push_back(t);
   pending_ = (int)launches_.size() - 1;
@@ -199,6 +214,7 @@ void Call::alloc_csr_result(stam_csr_result* r, int64_t nrows, int64_t ncols,
   own->dev = d;
   stats_->bytes_allocated += (int64_t)(pos_b + idx_b + val_b);
   r->handle = own;
+  adopt_result(&r->handle);
   r->nrows = nrows;
   r->ncols = ncols;
   r->pos = (int64_t*)d;
@@ -274,8 +290,8 @@ void Call::finish_csr_result(stam_csr_result* r, int64_t nnz) {
   own->host = h;
   own->host_bytes = total ? total : 16;
   if (opts_.timing) {
-    d2h_start_ = ctx_->event_pool[ctx_->event_next++];
-    d2h_stop_ = ctx_->event_pool[ctx_->event_next++];
+    d2h_start_ = next_event();
+    d2h_stop_ = next_event();
     STAM_CUDA_CHECK(cudaEventRecord(d2h_start_, ctx_->stream));
   }
   char* hc = (char*)h;
@@ -309,6 +325,7 @@ void Call::alloc_dense_result(stam_dense_result* r, int64_t nrows, int64_t ncols
   own->dev = d;
   stats_->bytes_allocated += (int64_t)b;
   r->handle = own;
+  adopt_result(&r->handle);
   r->nrows = nrows;
   r->ncols = ncols;
   r->vals = (double*)d;
@@ -323,8 +340,8 @@ void Call::finish_dense_result(stam_dense_result* r) {
   own->host = h;
   own->host_bytes = b ? b : 16;
   if (opts_.timing) {
-    d2h_start_ = ctx_->event_pool[ctx_->event_next++];
-    d2h_stop_ = ctx_->event_pool[ctx_->event_next++];
+    d2h_start_ = next_event();
+    d2h_stop_ = next_event();
     STAM_CUDA_CHECK(cudaEventRecord(d2h_start_, ctx_->stream));
   }
   if (b) STAM_CUDA_CHECK(cudaMemcpyAsync(h, r->vals, b, cudaMemcpyDeviceToHost, ctx_->stream));
@@ -470,7 +487,16 @@ int stam_cuda_ctx_create(int device, stam_cuda_ctx** out) {
     c->smem_optin = prop.sharedMemPerBlockOptin;
     STAM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
-    STAM_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&c->pool, device));
+    // a private stream-ordered pool: results and per-call temporaries are
+    // recycled without touching the OS allocator, and the device's default
+    // pool (shared with every other library in the process) stays as it was
+    cudaMemPoolProps pp;
+    std::memset(&pp, 0, sizeof(pp));
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    STAM_CUDA_CHECK(cudaMemPoolCreate(&c->pool, &pp));
     uint64_t threshold = UINT64_MAX;
     STAM_CUDA_CHECK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     STAM_CUDA_CHECK(cudaMallocHost(&c->h_scalars, 64 * sizeof(int64_t)));
@@ -496,6 +522,8 @@ int stam_cuda_ctx_destroy(stam_cuda_ctx* ctx) {
     if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     if (ctx->h_marks) cudaFreeHost(ctx->h_marks);
+    // results still held by the caller keep the pool alive until released
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     delete ctx;
   });
 }

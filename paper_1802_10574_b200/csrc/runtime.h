@@ -107,6 +107,9 @@ class Call {
   cudaEvent_t copy_fence();
   void wait(cudaEvent_t ev);
   cudaEvent_t event();
+  // Every event acquisition goes through here: grows the context's pool
+  // (timing-capable events) when a call needs more than it holds.
+  cudaEvent_t next_event();
 
   // Launch bookkeeping: call before/after each kernel launch.
   void before_launch(const char* name, cudaStream_t st = nullptr);
@@ -145,6 +148,12 @@ class Call {
  private:
   const void* stage(const void* p, size_t bytes, int32_t mem);
   void* pinned_alloc(size_t bytes);
+  void pinned_recycle(void* p, size_t bytes);
+  // The result allocated by this call: released by the destructor unless
+  // finish() succeeded (a call that fails after allocating its result must
+  // not hand the caller a handle it has no reason to release).
+  void adopt_result(void** handle_slot);
+  void** result_slot_ = nullptr;
 
   Ctx* ctx_;
   stam_options opts_;

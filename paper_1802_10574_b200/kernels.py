@@ -31,6 +31,9 @@ class _Owner:
     def __del__(self):
         try:
             if self.handle and self.ctx._ctx:
+                # free in order after torch work already queued on the stream
+                # the caller is using (results are read through torch tensors)
+                self.ctx._follow_torch()
                 N.load().stam_cuda_release(self.ctx._ctx, C.c_void_p(self.handle))
         except Exception:
             pass
@@ -68,7 +71,13 @@ def _host_copy(ptr: int, n: int, dtype) -> np.ndarray:
 
 
 class Context:
-    """One device + stream + memory pool (``stam_cuda_ctx``)."""
+    """One device + stream + memory pool (``stam_cuda_ctx``).
+
+    Stream ordering: unless ``set_stream`` pins a stream, every call (and every
+    release of a device result) runs on torch's *current* stream of the
+    context's device, so CUDA-tensor inputs produced by queued torch kernels
+    are complete before the library reads them, and a result's memory goes
+    back to the pool only after torch work queued on that stream."""
 
     def __init__(self, device: int = 0):
         self._lib = N.load()
@@ -76,6 +85,23 @@ class Context:
         N.check(self._lib.stam_cuda_ctx_create(int(device), C.byref(h)))
         self._ctx = h
         self.device = device
+        self._pinned_stream = False
+        self._cur_stream = None
+
+    def _follow_torch(self) -> None:
+        if self._pinned_stream or not self._ctx:
+            return
+        import sys
+
+        torch = sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_initialized():
+            return
+        raw = int(torch.cuda.current_stream(self.device).cuda_stream)
+        if raw == 0:
+            raw = 1  # torch's default stream is the legacy stream (cudaStreamLegacy)
+        if raw != self._cur_stream:
+            N.check(self._lib.stam_cuda_ctx_set_stream(self._ctx, C.c_void_p(raw)))
+            self._cur_stream = raw
 
     def close(self) -> None:
         if self._ctx:
@@ -92,6 +118,8 @@ class Context:
         """Run on a torch.cuda.Stream (or a raw cudaStream_t int); None resets."""
         raw = 0 if stream is None else int(getattr(stream, "cuda_stream", stream))
         N.check(self._lib.stam_cuda_ctx_set_stream(self._ctx, C.c_void_p(raw)))
+        self._pinned_stream = stream is not None
+        self._cur_stream = raw if stream is not None else None
 
     def synchronize(self) -> None:
         N.check(self._lib.stam_cuda_synchronize(self._ctx))
@@ -135,6 +163,7 @@ class Context:
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(sort, result, timing, self._MODES[mode])
+        self._follow_torch()
         N.check(self._lib.stam_cuda_spgemm(self._ctx, C.byref(A.view()), C.byref(B.view()),
                                            C.byref(opts), C.byref(r), C.byref(st)))
         return self._csr_out(r)
@@ -148,6 +177,7 @@ class Context:
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(sort, result, timing, N.STAM_MODE_COMPUTE)
+        self._follow_torch()
         N.check(self._lib.stam_cuda_spgemm_compute(
             self._ctx, C.byref(A.view()), C.byref(B.view()), C.byref(index.view()),
             C.byref(opts), C.byref(r), C.byref(st)))
@@ -164,6 +194,7 @@ class Context:
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(sort, result, timing, self._MODES[mode])
+        self._follow_torch()
         N.check(self._lib.stam_cuda_spadd(self._ctx, len(ops), views, C.byref(opts), C.byref(r),
                                           C.byref(st)))
         return self._csr_out(r)
@@ -176,6 +207,7 @@ class Context:
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(sort, result, timing, N.STAM_MODE_COMPUTE)
+        self._follow_torch()
         N.check(self._lib.stam_cuda_spadd_compute(self._ctx, len(ops), views,
                                                   C.byref(index.view()), C.byref(opts),
                                                   C.byref(r), C.byref(st)))
@@ -189,6 +221,7 @@ class Context:
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(True, result, timing)
+        self._follow_torch()
         N.check(self._lib.stam_cuda_ttv(self._ctx, C.byref(B.view()), C.byref(cv.view()),
                                         C.byref(opts), C.byref(r), C.byref(st)))
         return self._csr_out(r)
@@ -199,6 +232,7 @@ class Context:
         r = N.DenseResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(True, result, timing)
+        self._follow_torch()
         N.check(self._lib.stam_cuda_rowdot(self._ctx, C.byref(B.view()), C.byref(Cm.view()),
                                            C.byref(opts), C.byref(r), C.byref(st)))
         return self._dense_out(r)
@@ -210,6 +244,7 @@ class Context:
         r = N.CsrResult()
         st = stats if stats is not None else N.Stats()
         opts = self.options(True, result, timing)
+        self._follow_torch()
         N.check(self._lib.stam_cuda_spadd_merge(self._ctx, len(ops), views, C.byref(opts),
                                                 C.byref(r), C.byref(st)))
         return self._csr_out(r)
@@ -221,12 +256,14 @@ class Context:
         opts = self.options(True, result, timing)
         if isinstance(Cf, Dense) and isinstance(Df, Dense):
             r = N.DenseResult()
+            self._follow_torch()
             N.check(self._lib.stam_cuda_mttkrp_dense(
                 self._ctx, C.byref(B.view()), C.byref(Cf.view()), C.byref(Df.view()),
                 C.byref(opts), C.byref(r), C.byref(st)))
             return self._dense_out(r)
         if isinstance(Cf, CSR) and isinstance(Df, CSR):
             r = N.CsrResult()
+            self._follow_torch()
             N.check(self._lib.stam_cuda_mttkrp_sparse(
                 self._ctx, C.byref(B.view()), C.byref(Cf.view()), C.byref(Df.view()),
                 C.byref(opts), C.byref(r), C.byref(st)))
