@@ -2,9 +2,11 @@
 """Benchmark of the hot path.
 
 One "step" = one call of the kernel entry point (C ABI) over one batch of
-synthetic input with BASELINE.json's shapes.  Default workload: BASELINE
-configs[1] (config 2, SpAdd D = A+B+C, 3 x 200k x 200k, 50/row); ``--config``
-selects any of the five.
+synthetic input with BASELINE.json's shapes.  With no ``--config`` every one of
+BASELINE's five configs is measured and reported in ``configs``; the headline
+fields (``value``, ``roofline``, ``e2e``, ``cpu_baseline``) are those of the
+largest single-GPU config, config 5 (sparse-result MTTKRP, 7.2 GB per call).
+``--config K`` measures config K alone and makes it the headline.
 
 Our arm (default):
   value    = algorithmic HBM bytes of the call (inputs read once + output written
@@ -12,17 +14,22 @@ Our arm (default):
              inputs resident in HBM; whole-job aggregate over ranks.
   e2e      = the same metric through the same C-ABI call with pinned HOST
              inputs and a HOST result (H2D + D2H inside the timed region).
-  roofline = dominant kernel's algorithmic bytes / its CUDA-event duration vs
-             the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  roofline = the call's algorithmic bytes / its kernels' CUDA-event durations
+             vs the measured HBM copy bandwidth (MEASURED_PEAKS.json).
   cpu_baseline = the reference CPU path (oracle/_ref: the reference's own
-             Workspace/TensorBuilder) on the host cores, bounded sample.
+             Workspace/TensorBuilder) on the host: 1 thread (SPEC.md:425-426,
+             PAPER.md:1484-1486) and all host threads, median of 5 after a
+             discarded warm-up, bounded row/slice sample.
 
-``--impl reference``: rank 0 times the reference CPU path alone on the same
-config/metric (other ranks exit), printing the same JSON line.
+``--impl reference``: rank 0 times the reference CPU path alone on the
+headline config/metric (other ranks exit), printing the same JSON line.
 
-Multi-GPU (torchrun): weak scaling — every rank processes its own full-size
-shard of the row (slice) dimension with independently seeded inputs; no
-collective on the data path; time = max over ranks.
+Multi-GPU (torchrun, N ranks): STRONG scaling on one problem.  Rank 0
+generates the problem; the operand every rank reads in full (SpGEMM's B, the
+MTTKRP factors) is broadcast once over NCCL (``broadcast_ms``, outside the
+step), row / fiber / slice blocks are scattered once (sharding.py); a step is
+every rank's call on its block (+ the dense MTTKRP's boundary-row all-gather);
+time = max over ranks.
 """
 from __future__ import annotations
 
@@ -45,6 +52,7 @@ sys.path.insert(0, str(ROOT))
 L2_BYTES = 126e6
 METRIC = "SpGEMM/SpAdd/MTTKRP useful GFLOP/s; achieved HBM GB/s vs B200 peak"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+HEADLINE = 5               # largest single-GPU config (7.2 GB algorithmic per call)
 
 
 def _peak_hbm():
@@ -66,9 +74,6 @@ def _traffic(workload: str, kernel: str):
         return None
 
 
-# ---------------------------------------------------------------------------
-# workloads
-# ---------------------------------------------------------------------------
 def _csr_bytes(m) -> int:
     return 8 * (m.nrows + 1) + 16 * m.nnz
 
@@ -77,53 +82,110 @@ def _csf_bytes(b) -> int:
     return 8 * (b.dims[0] + 1) + 8 * b.nfibers + 8 * (b.nfibers + 1) + 16 * b.nnz
 
 
+def _pin(a):
+    """Pinned host copy of a (host or device) array."""
+    import torch
+
+    t = a if type(a).__module__.startswith("torch") else torch.from_numpy(np.ascontiguousarray(a))
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h
+
+
+def _sync():
+    import torch
+
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
 class Workload:
-    """Common driver: inputs on device, raw C-ABI step, e2e step, CPU ref."""
+    """Inputs on device (the rank's block), raw C-ABI step, e2e step, CPU ref.
+
+    Rank 0 generates the whole problem (``cfg``); ``distribute`` leaves every
+    rank with its block resident on its GPU (``dist_on`` False: one process,
+    the whole problem)."""
 
     mode = "fused"  # fused | assemble | compute | unsorted (SpGEMM, SpAdd)
 
-    def __init__(self, cid: int, shard: int):
+    def __init__(self, cid: int, have_data: bool = True):
         from paper_1802_10574_b200 import generators as G
 
         self.cid = cid
         self.name = G.CONFIG_NAMES[cid]
-        t = time.time()
-        self.cfg = G.make_config(cid, shard=shard)
-        self.gen_s = time.time() - t
+        self.cfg = None
+        self.gen_s = 0.0
+        if have_data:
+            t = time.time()
+            self.cfg = G.make_config(cid)
+            self.gen_s = time.time() - t
+        self.broadcast_ms = 0.0
+        self.broadcast_bytes = 0
 
-    # populated by subclasses
-    def setup(self, ctx):
-        raise NotImplementedError
+    def _bcast(self, fn):
+        """Runs a broadcast, timing it (device-synchronised wall clock)."""
+        _sync()
+        t = time.perf_counter()
+        out = fn()
+        _sync()
+        self.broadcast_ms += (time.perf_counter() - t) * 1e3
+        return out
 
-    def step(self, timing=False):
-        raise NotImplementedError
+    def _init_native(self, ctx):
+        from paper_1802_10574_b200 import _native as N
 
-    def e2e_step(self):
-        raise NotImplementedError
+        self.N, self.ctx, self.lib = N, ctx, N.load()
+
+    def release(self, r):
+        self.N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
+
+    def post_step(self, r):
+        """Data-path exchange after the call (dense MTTKRP at N > 1)."""
+
+    def algo_bytes_total(self, dist_on):
+        """Whole-problem algorithmic bytes: every rank's own block inputs and
+        outputs + the broadcast operand once."""
+        own = self.own_in_bytes + self.out_bytes
+        if dist_on:
+            import torch
+            import torch.distributed as dist
+
+            t = torch.tensor([float(own)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t)
+            own = float(t.item())
+        return own + self.shared_bytes
 
 
 class SpaddWork(Workload):
+    def distribute(self, world, rank, dist_on):
+        from paper_1802_10574_b200 import sharding as S
+
+        if not dist_on:
+            self.local = [o.to("cuda") for o in self.cfg["ops"]]
+        else:
+            ops = self.cfg["ops"] if rank == 0 else None
+            nops = int(S.broadcast_ints([len(ops)] if rank == 0 else None, 1, "cuda")[0])
+            w = sum(np.diff(o.pos) for o in ops) if rank == 0 else None
+            bounds = S.broadcast_ints(S.balanced_bounds(w, world) if rank == 0 else None,
+                                      world + 1, "cuda")
+            self.local = [S.scatter_csr_rows(ops[q] if rank == 0 else None, bounds, "cuda")
+                          for q in range(nops)]
+            self.row0 = int(bounds[rank])
+        self.own_in_bytes = sum(_csr_bytes(o) for o in self.local)
+        self.shared_bytes = 0
+        self.local_adds = sum(o.nnz for o in self.local[1:])
+
     def setup(self, ctx):
-        from paper_1802_10574_b200 import _native as N
-
-        self.N = N
-        self.ctx = ctx
-        self.lib = N.load()
-        self.dev = [o.to("cuda") for o in self.cfg["ops"]]
-        self.views = (N.CsrView * len(self.dev))(*[o.view() for o in self.dev])
-        import torch
-
-        self.pinned = []
-        for o in self.cfg["ops"]:
-            arrs = [torch.from_numpy(a).pin_memory() for a in (o.pos, o.idx, o.vals)]
-            self.pinned.append(arrs)
         from paper_1802_10574_b200.storage import CSR
 
-        hops = [CSR(o.nrows, o.ncols, *arrs) for o, arrs in zip(self.cfg["ops"], self.pinned)]
-        self.hviews = (N.CsrView * len(hops))(*[h.view() for h in hops])
-        for v in self.hviews:
-            v.mem = N.STAM_MEM_HOST
-        self.in_bytes = sum(_csr_bytes(o) for o in self.cfg["ops"])
+        self._init_native(ctx)
+        N = self.N
+        self.views = (N.CsrView * len(self.local))(*[o.view() for o in self.local])
+        self.hops = [CSR(o.nrows, o.ncols, _pin(o.pos), _pin(o.idx), _pin(o.vals))
+                     for o in self.local]
+        self.hviews = (N.CsrView * len(self.hops))(*[h.view() for h in self.hops])
         self.nnz_out = None
 
     def _index(self, views):
@@ -132,7 +194,7 @@ class SpaddWork(Workload):
             N = self.N
             r = N.CsrResult()
             opts = N.Options(1, N.STAM_MODE_ASSEMBLE, N.STAM_MEM_DEVICE, 0)
-            N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.dev), self.views,
+            N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.local), self.views,
                                              C.byref(opts), C.byref(r), C.byref(N.Stats())))
             self._idx = r
             self._idx_view = N.CsrView(r.nrows, r.ncols, r.nnz, r.pos, r.idx, r.vals,
@@ -149,15 +211,14 @@ class SpaddWork(Workload):
                          1 if timing else 0)
         if self.mode == "compute":
             N.check(self.lib.stam_cuda_spadd_compute(
-                self.ctx._ctx, len(self.dev), views, C.byref(self._index(views)), C.byref(opts),
-                C.byref(r), C.byref(st)))
+                self.ctx._ctx, len(self.local), views, C.byref(self._index(views)),
+                C.byref(opts), C.byref(r), C.byref(st)))
         else:
-            N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.dev), views, C.byref(opts),
-                                             C.byref(r), C.byref(st)))
-        nnz, nrows = r.nnz, r.nrows
-        N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
-        self.nnz_out = nnz
-        self.out_bytes = 8 * (nrows + 1) + 16 * nnz
+            N.check(self.lib.stam_cuda_spadd(self.ctx._ctx, len(self.local), views,
+                                             C.byref(opts), C.byref(r), C.byref(st)))
+        self.nnz_out = r.nnz
+        self.out_bytes = 8 * (r.nrows + 1) + 16 * r.nnz
+        self.release(r)
         return st
 
     def step(self, timing=False):
@@ -166,22 +227,21 @@ class SpaddWork(Workload):
     def e2e_step(self):
         return self._call(self.hviews, self.N.STAM_MEM_HOST, False)
 
-    def algo_bytes(self):
-        return self.in_bytes + self.out_bytes
-
-    def flops(self):
+    def local_flops(self):
         # workspace adds executed (SPEC counters: every accumulate insert)
-        return sum(o.nnz for o in self.cfg["ops"][1:])
+        return self.local_adds
 
     def h2d_bytes(self):
-        return self.in_bytes
+        return self.own_in_bytes
 
     def d2h_bytes(self):
         return self.out_bytes
 
-    # reference CPU path on a row sample
+    # reference CPU path on a row sample (rank 0, whole problem)
+    def total_units(self):
+        return self.cfg["ops"][0].nrows
+
     def ref_sample(self, rows):
-        import numpy as np
         from paper_1802_10574_b200.storage import CSR
 
         sub = []
@@ -197,31 +257,52 @@ class SpaddWork(Workload):
         return sum(_csr_bytes(o) for o in sample) + 8 * (out["nrows"] + 1) + 16 * int(
             out["pos"][-1]), sum(o.nnz for o in sample[1:])
 
-    def total_rows(self):
-        return self.cfg["ops"][0].nrows
-
 
 class SpgemmWork(Workload):
     """C = A*B (configs 1 and 3; config 3 squares A, so B is A)."""
 
-    def setup(self, ctx):
-        from paper_1802_10574_b200 import _native as N
-        from paper_1802_10574_b200.storage import CSR
+    def distribute(self, world, rank, dist_on):
         import torch
 
-        self.N, self.ctx, self.lib = N, ctx, N.load()
-        A, B = self.cfg["A"], self.cfg["B"]
-        self.same = B is A
-        self.Ad = A.to("cuda")
-        self.Bd = self.Ad if self.same else B.to("cuda")
-        self.va, self.vb = self.Ad.view(), self.Bd.view()
-        pin = lambda m: CSR(m.nrows, m.ncols, *[torch.from_numpy(a).pin_memory()
-                                                for a in (m.pos, m.idx, m.vals)])
-        self.Ah = pin(A)
-        self.Bh = self.Ah if self.same else pin(B)
+        from paper_1802_10574_b200 import sharding as S
+
+        if not dist_on:
+            A, B = self.cfg["A"], self.cfg["B"]
+            self.same = B is A
+            self.Al = A.to("cuda")
+            self.Bd = self.Al if self.same else B.to("cuda")
+            self.own_in_bytes = _csr_bytes(A)
+            self.shared_bytes = 0 if self.same else _csr_bytes(B)
+        else:
+            A = self.cfg["A"] if rank == 0 else None
+            B = self.cfg["B"] if rank == 0 else None
+            self.same = bool(S.broadcast_ints([int(B is A)] if rank == 0 else None, 1, "cuda")[0])
+            bounds = S.broadcast_ints(
+                S.balanced_bounds(S.spgemm_row_weights(A, B), world) if rank == 0 else None,
+                world + 1, "cuda")
+            # B broadcast once over NVLink (for A·A this is A itself)
+            self.Bd = self._bcast(lambda: S.broadcast_csr(B, 0, "cuda"))
+            self.broadcast_bytes = _csr_bytes(self.Bd)
+            r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+            self.row0 = r0
+            self.Al = (S.device_rows(self.Bd, r0, r1) if self.same
+                       else S.scatter_csr_rows(A, bounds, "cuda"))
+            # A·A: A's bytes are the broadcast operand's (counted once)
+            self.own_in_bytes = 0 if self.same else _csr_bytes(self.Al)
+            self.shared_bytes = _csr_bytes(self.Bd)
+        blen = self.Bd.pos[1:] - self.Bd.pos[:-1]
+        self.local_products = int(blen[self.Al.idx].sum().item()) if self.Al.nnz else 0
+        torch.cuda.synchronize()
+
+    def setup(self, ctx):
+        from paper_1802_10574_b200.storage import CSR
+
+        self._init_native(ctx)
+        self.va, self.vb = self.Al.view(), self.Bd.view()
+        pin = lambda m: CSR(m.nrows, m.ncols, _pin(m.pos), _pin(m.idx), _pin(m.vals))
+        self.Ah = pin(self.Al)
+        self.Bh = self.Ah if (self.same and self.Al.nrows == self.Bd.nrows) else pin(self.Bd)
         self.ha, self.hb = self.Ah.view(), self.Bh.view()
-        self.in_bytes = _csr_bytes(A) + (0 if self.same else _csr_bytes(B))
-        self.products = int(np.sum(np.diff(B.pos)[A.idx]))
         self.nnz_out = None
 
     def _index(self):
@@ -254,7 +335,7 @@ class SpgemmWork(Workload):
                                               C.byref(opts), C.byref(r), C.byref(st)))
         self.nnz_out = r.nnz
         self.out_bytes = 8 * (r.nrows + 1) + 16 * r.nnz
-        N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
+        self.release(r)
         return st
 
     def step(self, timing=False):
@@ -263,17 +344,17 @@ class SpgemmWork(Workload):
     def e2e_step(self):
         return self._call(self.ha, self.hb, self.N.STAM_MEM_HOST, False)
 
-    def algo_bytes(self):
-        return self.in_bytes + self.out_bytes
-
-    def flops(self):
-        return 2 * self.products
+    def local_flops(self):
+        return 2 * self.local_products
 
     def h2d_bytes(self):
-        return self.in_bytes
+        return _csr_bytes(self.Al) + (0 if self.Bh is self.Ah else _csr_bytes(self.Bd))
 
     def d2h_bytes(self):
         return self.out_bytes
+
+    def total_units(self):
+        return self.cfg["A"].nrows
 
     def ref_sample(self, rows):
         from paper_1802_10574_b200.storage import CSR
@@ -287,43 +368,81 @@ class SpgemmWork(Workload):
 
         A, B = sample
         out = oracle.ref_spgemm(A, B, nthreads)
-        nbytes = _csr_bytes(A) + (0 if self.same else _csr_bytes(B)) + 8 * (out["nrows"] + 1) + \
+        same = self.cfg["B"] is self.cfg["A"]
+        nbytes = _csr_bytes(A) + (0 if same else _csr_bytes(B)) + 8 * (out["nrows"] + 1) + \
             16 * int(out["pos"][-1])
         return nbytes, 2 * int(np.sum(np.diff(B.pos)[A.idx]))
-
-    def total_rows(self):
-        return self.cfg["A"].nrows
 
 
 class MttkrpWork(Workload):
     """A = B x_2 C x_3 D: dense factors (config 4) or CSR factors (config 5)."""
 
-    def setup(self, ctx):
-        from paper_1802_10574_b200 import _native as N
-        from paper_1802_10574_b200.storage import CSF3, CSR, Dense
+    def distribute(self, world, rank, dist_on):
         import torch
 
-        self.N, self.ctx, self.lib = N, ctx, N.load()
-        B, Cf, Df = self.cfg["B"], self.cfg["C"], self.cfg["D"]
-        self.dense = isinstance(Cf, Dense)
-        self.Bd, self.Cd, self.Dd = B.to("cuda"), Cf.to("cuda"), Df.to("cuda")
-        self.vB, self.vC, self.vD = self.Bd.view(), self.Cd.view(), self.Dd.view()
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        self.Bh = CSF3(B.dims, *[pin(a) for a in (B.pos1, B.idx1, B.pos2, B.idx2, B.vals)])
+        from paper_1802_10574_b200 import sharding as S
+        from paper_1802_10574_b200.storage import Dense
+
+        self.dist_on = dist_on
+        if not dist_on:
+            B, Cf, Df = self.cfg["B"], self.cfg["C"], self.cfg["D"]
+            self.dense = isinstance(Cf, Dense)
+            self.Bl, self.Cd, self.Dd = B.to("cuda"), Cf.to("cuda"), Df.to("cuda")
+            self.spans = None
+        else:
+            cfg = self.cfg
+            self.dense = bool(S.broadcast_ints(
+                [int(isinstance(cfg["C"], Dense))] if rank == 0 else None, 1, "cuda")[0])
+            B = cfg["B"] if rank == 0 else None
+            if self.dense:
+                fb = S.broadcast_ints(S.fiber_bounds(B, world) if rank == 0 else None,
+                                      world + 1, "cuda")
+                self.Cd = Dense(self._bcast(lambda: S.broadcast_dense(
+                    cfg["C"].vals if rank == 0 else None, 0, "cuda")))
+                self.Dd = Dense(self._bcast(lambda: S.broadcast_dense(
+                    cfg["D"].vals if rank == 0 else None, 0, "cuda")))
+                self.s0, _, self.spans, self.Bl = S.scatter_csf_fibers(B, fb, "cuda")
+            else:
+                if rank == 0:
+                    pos1, pos2 = B.pos1, B.pos2
+                    bounds = S.balanced_bounds(np.diff(pos2[pos1]), world)
+                bounds = S.broadcast_ints(bounds if rank == 0 else None, world + 1, "cuda")
+                self.Cd = self._bcast(lambda: S.broadcast_csr(cfg["C"] if rank == 0 else None,
+                                                               0, "cuda"))
+                self.Dd = self._bcast(lambda: S.broadcast_csr(cfg["D"] if rank == 0 else None,
+                                                               0, "cuda"))
+                self.Bl = S.scatter_csf_slices(B, bounds, "cuda")
+                self.spans = None
+                self.s0 = int(bounds[rank])
         if self.dense:
-            self.Ch, self.Dh = Dense(pin(Cf.vals)), Dense(pin(Df.vals))
-            self.in_bytes = _csf_bytes(B) + 8 * (Cf.vals.size + Df.vals.size)
-            self.R = Cf.ncols
-            self.useful = 2 * self.R * (B.nnz + B.nfibers)
+            self.R = int(self.Cd.vals.shape[1])
+            self.shared_bytes = 8 * (self.Cd.vals.numel() + self.Dd.vals.numel())
+            self.useful = 2 * self.R * (self.Bl.nnz + self.Bl.nfibers)
             # every nonzero reads a factor row of D and every fiber one of C:
             # the loop nest's operand stream from L2 (SURVEY P6)
-            self.l2_gather = 8 * self.R * (B.nnz + B.nfibers)
+            self.l2_gather = 8 * self.R * (self.Bl.nnz + self.Bl.nfibers)
         else:
-            self.Ch = CSR(Cf.nrows, Cf.ncols, *[pin(a) for a in (Cf.pos, Cf.idx, Cf.vals)])
-            self.Dh = CSR(Df.nrows, Df.ncols, *[pin(a) for a in (Df.pos, Df.idx, Df.vals)])
-            self.in_bytes = _csf_bytes(B) + _csr_bytes(Cf) + _csr_bytes(Df)
-            self.R = Cf.ncols
+            self.R = self.Cd.ncols
+            self.shared_bytes = _csr_bytes(self.Cd) + _csr_bytes(self.Dd)
             self.useful = None
+        self.broadcast_bytes = self.shared_bytes if dist_on else 0
+        self.own_in_bytes = _csf_bytes(self.Bl)
+        torch.cuda.synchronize()
+
+    def setup(self, ctx):
+        from paper_1802_10574_b200.storage import CSF3, CSR, Dense
+
+        self._init_native(ctx)
+        self.vB, self.vC, self.vD = self.Bl.view(), self.Cd.view(), self.Dd.view()
+        B = self.Bl
+        self.Bh = CSF3(B.dims, *[_pin(a) for a in (B.pos1, B.idx1, B.pos2, B.idx2, B.vals)])
+        if self.dense:
+            self.Ch, self.Dh = Dense(_pin(self.Cd.vals)), Dense(_pin(self.Dd.vals))
+        else:
+            self.Ch = CSR(self.Cd.nrows, self.Cd.ncols,
+                          *[_pin(a) for a in (self.Cd.pos, self.Cd.idx, self.Cd.vals)])
+            self.Dh = CSR(self.Dd.nrows, self.Dd.ncols,
+                          *[_pin(a) for a in (self.Dd.pos, self.Dd.idx, self.Dd.vals)])
         self.hB, self.hC, self.hD = self.Bh.view(), self.Ch.view(), self.Dh.view()
         self.nnz_out = None
 
@@ -338,6 +457,8 @@ class MttkrpWork(Workload):
                                                     C.byref(st)))
             self.out_bytes = 8 * r.nrows * r.ncols
             self.nnz_out = r.nrows * r.ncols
+            if result_mem == N.STAM_MEM_DEVICE:
+                self.post_step(r)
         else:
             r = N.CsrResult()
             N.check(self.lib.stam_cuda_mttkrp_sparse(self.ctx._ctx, C.byref(vB), C.byref(vC),
@@ -346,8 +467,22 @@ class MttkrpWork(Workload):
             self.out_bytes = 8 * (r.nrows + 1) + 16 * r.nnz
             self.nnz_out = r.nnz
             self._sparse_mults = st.mults
-        N.check(self.lib.stam_cuda_release(self.ctx._ctx, C.c_void_p(r.handle)))
+        self.release(r)
         return st
+
+    def post_step(self, r):
+        """Dense result at N > 1: the cut slices' partial rows are completed
+        by one all-gather (sharding.exchange_boundary_rows), in the step."""
+        if not self.dist_on or self.spans is None:
+            return
+        from paper_1802_10574_b200 import sharding as S
+        from paper_1802_10574_b200.kernels import _dev_tensor
+
+        n = r.nrows * r.ncols
+        if n == 0:
+            return
+        t = _dev_tensor(r.vals, n, "float64", None).view(r.nrows, r.ncols)
+        S.exchange_boundary_rows(t, self.spans, "cuda")
 
     def step(self, timing=False):
         return self._call(self.vB, self.vC, self.vD, self.N.STAM_MEM_DEVICE, timing)
@@ -355,19 +490,19 @@ class MttkrpWork(Workload):
     def e2e_step(self):
         return self._call(self.hB, self.hC, self.hD, self.N.STAM_MEM_HOST, False)
 
-    def algo_bytes(self):
-        return self.in_bytes + self.out_bytes
-
-    def flops(self):
+    def local_flops(self):
         if self.useful is not None:
             return self.useful
         return 2 * getattr(self, "_sparse_mults", 0)
 
     def h2d_bytes(self):
-        return self.in_bytes
+        return self.own_in_bytes + self.shared_bytes
 
     def d2h_bytes(self):
         return self.out_bytes
+
+    def total_units(self):
+        return self.cfg["B"].dims[0]
 
     def ref_sample(self, slices):
         from paper_1802_10574_b200.storage import CSF3
@@ -375,25 +510,23 @@ class MttkrpWork(Workload):
         B = self.cfg["B"]
         f = int(B.pos1[slices])
         z = int(B.pos2[f])
-        sub = CSF3((slices, B.dims[1], B.dims[2]), B.pos1[: slices + 1], B.idx1[:f],
-                   B.pos2[: f + 1], B.idx2[:z], B.vals[:z])
-        return sub
+        return CSF3((slices, B.dims[1], B.dims[2]), B.pos1[: slices + 1], B.idx1[:f],
+                    B.pos2[: f + 1], B.idx2[:z], B.vals[:z])
 
     def ref_run(self, sub, nthreads):
         import oracle
 
-        if self.dense:
-            oracle.ref_mttkrp_dense(sub, self.cfg["C"].vals, self.cfg["D"].vals, nthreads)
-            nbytes = _csf_bytes(sub) + 8 * (self.cfg["C"].vals.size + self.cfg["D"].vals.size) + \
-                8 * sub.dims[0] * self.R
-            return nbytes, 2 * self.R * (sub.nnz + sub.nfibers)
-        out = oracle.ref_mttkrp_sparse(sub, self.cfg["C"], self.cfg["D"], nthreads)
-        nbytes = _csf_bytes(sub) + _csr_bytes(self.cfg["C"]) + _csr_bytes(self.cfg["D"]) + \
+        cfg = self.cfg
+        if isinstance(cfg["C"].vals, np.ndarray) and cfg["C"].vals.ndim == 2:
+            oracle.ref_mttkrp_dense(sub, cfg["C"].vals, cfg["D"].vals, nthreads)
+            R = cfg["C"].vals.shape[1]
+            nbytes = _csf_bytes(sub) + 8 * (cfg["C"].vals.size + cfg["D"].vals.size) + \
+                8 * sub.dims[0] * R
+            return nbytes, 2 * R * (sub.nnz + sub.nfibers)
+        out = oracle.ref_mttkrp_sparse(sub, cfg["C"], cfg["D"], nthreads)
+        nbytes = _csf_bytes(sub) + _csr_bytes(cfg["C"]) + _csr_bytes(cfg["D"]) + \
             8 * (out["nrows"] + 1) + 16 * int(out["pos"][-1])
         return nbytes, 0
-
-    def total_rows(self):
-        return self.cfg["B"].dims[0]
 
 
 WORKLOADS = {1: SpgemmWork, 2: SpaddWork, 3: SpgemmWork, 4: MttkrpWork, 5: MttkrpWork}
@@ -407,6 +540,7 @@ class FileSpgemmWork(SpgemmWork):
 
         self.cid = 0
         self.name = f"file:{Path(path).name}:AxA"
+        self.broadcast_ms, self.broadcast_bytes = 0.0, 0
         t = time.time()
         A = sio.load_matrix_market(path)
         if A.nrows != A.ncols:
@@ -425,6 +559,7 @@ class FileMttkrpWork(MttkrpWork):
 
         self.cid = 0
         self.name = f"file:{Path(path).name}:R{rank}"
+        self.broadcast_ms, self.broadcast_bytes = 0.0, 0
         t = time.time()
         B = sio.load_tns(path)
         if not hasattr(B, "pos1"):
@@ -462,9 +597,6 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
 
-    def mark(self):
-        return time.time()
-
     def stop(self, t0, t1):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -494,27 +626,72 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# reference CPU path
+# ---------------------------------------------------------------------------
+def _ref_kind():
+    import oracle
+
+    if not oracle.ref_available():
+        raise SystemExit("oracle/_ref missing; run __graft_entry__.build() where /root/reference "
+                         "exists")
+    return "reference"
+
+
+def ref_timed(W, nthreads, target_s, reps=5):
+    """The reference CPU path on a bounded sample of W's rows/slices: one
+    discarded warm-up, then the median of `reps` timed runs.
+    Returns (GB/s, useful GFLOP/s, units, seconds per run)."""
+    units = W.total_units()
+    t = time.perf_counter()
+    probe = max(1, units // 200)
+    W.ref_run(W.ref_sample(probe), nthreads)
+    per_unit = (time.perf_counter() - t) / probe
+    n = int(min(units, max(1, target_s / max(per_unit, 1e-9))))
+    sample = W.ref_sample(n)
+    W.ref_run(sample, nthreads)  # warm-up, discarded
+    times = []
+    nbytes = flops = 0
+    for _ in range(reps):
+        t = time.perf_counter()
+        nbytes, flops = W.ref_run(sample, nthreads)
+        times.append(time.perf_counter() - t)
+    med = statistics.median(times)
+    return nbytes / med / 1e9, flops / med / 1e9, n, med
+
+
+def cpu_baselines(W, target_s):
+    kind = _ref_kind()
+    out = {}
+    cores = os.cpu_count() or 1
+    unit = "slices" if W.cid in (4, 5) else "rows"
+    for label, nt in (("1thread", 1), ("all", cores)):
+        v, g, n, med = ref_timed(W, nt, target_s)
+        out[label] = {"value": v, "unit": "GB/s", "useful_gflops": g or None, "cores": nt,
+                      "kind": kind,
+                      "sample": f"first {n} of {W.total_units()} {unit}, median of 5 runs "
+                                f"({med:.2f} s each) after a discarded warm-up; reference "
+                                f"Workspace/TensorBuilder, {nt} thread(s)"
+                                + (" (row blocks, one Workspace each)" if nt > 1 else "")}
+    return out
+
+
 def run_reference(args, cid):
-    """--impl reference: the reference CPU path alone, rank 0 only."""
+    """--impl reference: the reference CPU path alone, rank 0 only, all host
+    threads, each step a bounded sample of the workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
-
-    W = WORKLOADS[cid](cid, 0)
-    kind = "reference" if oracle.ref_available() else "port"
-    if kind != "reference":
-        raise SystemExit("oracle/_ref missing; run __graft_entry__.build() where /root/reference exists")
+    kind = _ref_kind()
+    W = WORKLOADS[cid](cid)
     nthreads = os.cpu_count() or 1
-    rows = W.total_rows()
-    # size the per-step sample so the whole run ends within a few minutes
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    units = W.total_units()
     t = time.perf_counter()
-    W.ref_run(W.ref_sample(max(1, rows // 20)), nthreads)
-    est_full = (time.perf_counter() - t) * 20
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    if est_full > budget:
-        rows = max(1, int(rows * budget / est_full))
-    sample = W.ref_sample(rows)
+    probe = max(1, units // 200)
+    W.ref_run(W.ref_sample(probe), nthreads)
+    per_unit = (time.perf_counter() - t) / probe
+    n = int(min(units, max(1, budget / max(per_unit, 1e-9))))
+    sample = W.ref_sample(n)
     for _ in range(args.warmup):
         W.ref_run(sample, nthreads)
     times, nbytes, flops = [], 0, 0
@@ -524,97 +701,35 @@ def run_reference(args, cid):
         times.append(time.perf_counter() - t)
     tot = sum(times)
     value = nbytes * args.steps / tot / 1e9
+    unit = "slices" if cid in (4, 5) else "rows"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": W.name, "config_id": cid, "sample_rows": rows,
-                   "total_rows": W.total_rows()},
-        "useful_gflops": flops * args.steps / tot / 1e9,
+        "config": {"workload": W.name, "config_id": cid, "sample_units": n,
+                   "total_units": units},
+        "useful_gflops": (flops * args.steps / tot / 1e9) or None,
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": nthreads, "kind": kind,
-                         "sample": f"first {rows} of {W.total_rows()} rows per step, "
-                                   f"{nthreads} threads (row blocks, one Workspace each)"},
+                         "sample": f"first {n} of {units} {unit} per step, {nthreads} threads "
+                                   f"(row blocks, one Workspace each)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(W, target_s=10.0):
-    import oracle
-
-    kind = "reference" if oracle.ref_available() else "port"
-    nthreads = os.cpu_count() or 1
-    rows = W.total_rows()
-    sample = W.ref_sample(rows)
-    reps, t_all, nbytes = 0, 0.0, 0
-    rates = []
-    while (t_all < target_s and reps < 5) or reps < 2:
-        t = time.perf_counter()
-        if kind == "reference":
-            nbytes, _ = W.ref_run(sample, nthreads)
-        dt = time.perf_counter() - t
-        rates.append(nbytes / dt / 1e9)
-        t_all += dt
-        reps += 1
-    return {"value": statistics.median(rates), "unit": "GB/s", "cores": nthreads, "kind": kind,
-            "sample": f"full config, {reps} repetitions, median; reference Workspace/"
-                      f"TensorBuilder over {nthreads} host threads (row blocks)"}
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mtx", help="SpGEMM A*A on this Matrix Market file instead of a config")
-    ap.add_argument("--tns", help="dense MTTKRP on this FROSTT .tns file instead of a config")
-    ap.add_argument("--rank", type=int, default=32, help="factor rank for --tns")
-    ap.add_argument("--mode", default="fused", choices=["fused", "assemble", "compute", "unsorted"],
-                    help="execution mode (SpGEMM / SpAdd configs): SPEC.md:372-374, sort flag :351")
-    args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
-    cid = args.config
-    if cid not in WORKLOADS:
-        raise SystemExit(f"config {cid} not available in this build")
-    if args.impl == "reference":
-        return run_reference(args, cid)
-
+# ---------------------------------------------------------------------------
+# one config on this rank
+# ---------------------------------------------------------------------------
+def run_config(W, args, ctx, stream, world, rank, dist_on, local, cpu_target_s):
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    from paper_1802_10574_b200 import Context
-
-    if args.mtx:
-        W = FileSpgemmWork(args.mtx)
-    elif args.tns:
-        W = FileMttkrpWork(args.tns, args.rank)
-    else:
-        W = WORKLOADS[cid](cid, rank)
-    if args.mode != "fused":
-        if cid not in (1, 2, 3) and not args.mtx:
-            raise SystemExit("--mode applies to the SpGEMM and SpAdd configs (1, 2, 3)")
-        W.mode = args.mode
-    ctx = Context(local)
-    stream = torch.cuda.Stream(device=local)
-    ctx.set_stream(stream)
+    W.distribute(world, rank, dist_on)
     W.setup(ctx)
-
-    # L2 is 126 MB: workloads whose inputs fit are timed with a flush (a
-    # 256 MB read-modify-write) before every step
     flush = (torch.zeros(32 << 20, dtype=torch.float64, device="cuda")
-             if W.in_bytes <= L2_BYTES else None)
+             if (W.own_in_bytes + W.shared_bytes) <= L2_BYTES else None)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -622,13 +737,13 @@ def main():
         for _ in range(args.warmup):
             W.step()
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
         launches = 0
         if flush is None:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
             t0 = time.time()
             ev0.record(stream)
             for _ in range(args.steps):
@@ -637,6 +752,7 @@ def main():
             ev1.record(stream)
             torch.cuda.synchronize()
             t1 = time.time()
+            ms = ev0.elapsed_time(ev1) / args.steps
         else:
             # inputs fit in L2: flush it before every step, time each step
             # with its own events (the flush is outside the timed region)
@@ -651,91 +767,192 @@ def main():
                 launches += st.kernel_launches
             torch.cuda.synchronize()
             t1 = time.time()
-        if world > 1:
+            ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
     clk = clocks.stop(t0, t1)
-    if flush is None:
-        ms = ev0.elapsed_time(ev1) / args.steps
-    else:
-        ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    # kernel timings (separate pass with per-kernel events)
+    # kernel timings (separate pass with per-kernel events recorded by the library)
     kms, tot_ms, kname = [], [], ""
     with torch.cuda.stream(stream):
-        for _ in range(max(5, min(args.steps, 50))):
+        for _ in range(max(5, min(args.steps, 30))):
             if flush is not None:
                 flush.add_(1)
             st = W.step(timing=True)
             kms.append(st.main_kernel_ms)
             tot_ms.append(st.total_kernel_ms)
             kname = st.main_kernel.decode()
-    kernel_ms = statistics.mean(kms)
     # e2e through the C ABI with pinned host buffers
     e2e_times = []
-    for _ in range(max(3, min(args.steps, 10))):
+    for _ in range(max(3, min(args.steps, 8))):
         torch.cuda.synchronize()
         t = time.perf_counter()
         W.e2e_step()
         e2e_times.append(time.perf_counter() - t)
     e2e_s = statistics.median(e2e_times)
 
-    algo = W.algo_bytes()
-    per_rank = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
+    algo = W.algo_bytes_total(dist_on)
+    flops = float(W.local_flops())
+    nnz_out = float(W.nnz_out)
+    per_rank = torch.tensor([ms, e2e_s, -flops, -nnz_out, float(W.broadcast_ms)],
+                            dtype=torch.float64, device="cuda")
+    if dist_on:
         dist.all_reduce(per_rank, op=dist.ReduceOp.MAX)
-    ms_max, e2e_max = per_rank.tolist()
-    value = algo * world / (ms_max * 1e-3) / 1e9
+        sums = torch.tensor([flops, nnz_out], dtype=torch.float64, device="cuda")
+        dist.all_reduce(sums)
+        flops, nnz_out = sums.tolist()
+    ms_max, e2e_max, _, _, bcast_ms = per_rank.tolist()
+    if rank != 0:
+        return None
     peak, peak_src = _peak_hbm()
-    # the call's algorithmic bytes over the device time of ALL its kernels
-    # (single-kernel calls: that kernel); the dominant kernel is named beside.
-    # Calls that run kernels on two streams at once (SpGEMM) overlap them, so
-    # the basis is the smaller of the kernel-duration sum and the step time.
+    # rank 0's own call: its algorithmic bytes over the device time of ALL its
+    # kernels (single-kernel calls: that kernel); the dominant kernel is named
+    # beside.  Calls that overlap kernels on two streams (SpGEMM) use the
+    # smaller of the kernel-duration sum and the step time.
+    own_algo = W.own_in_bytes + W.shared_bytes + W.out_bytes
+    kernel_ms = statistics.mean(kms)
     total_kms = statistics.mean(tot_ms)
     overlapped = total_kms > ms
     basis_ms = min(total_kms, ms)
-    achieved = algo / (basis_ms * 1e-3) / 1e9
+    achieved = own_algo / (basis_ms * 1e-3) / 1e9
+    res = {
+        "workload": W.name, "config_id": W.cid or None,
+        "value": algo / (ms_max * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_max,
+        "useful_gflops": flops / (ms_max * 1e-3) / 1e9,
+        "algo_bytes_per_step": algo, "nnz_out": int(nnz_out),
+        "l2": "inputs larger than L2 (no flush)" if flush is None
+              else "inputs smaller than L2: 256 MB L2 flush before every timed step",
+        "kernel_ms": kernel_ms, "kernels_total_ms": total_kms,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic(W.name, kname),
+                     "kernel": kname, "kernel_share": kernel_ms / total_kms if total_kms else None,
+                     "kernels_per_call": launches // max(1, args.steps),
+                     "time_basis": ("device step time (the call's kernels overlap on two "
+                                    "streams; their durations sum to %.3f ms)" % total_kms)
+                     if overlapped else "sum of the call's kernel durations (CUDA events)",
+                     "peak_source": peak_src,
+                     **({"l2_gather": {"bytes_per_step": W.l2_gather,
+                                       "achieved_gbs": W.l2_gather / (basis_ms * 1e-3) / 1e9,
+                                       "note": "factor rows read per nonzero / fiber "
+                                               "(L2-resident); the binding stream"}}
+                        if getattr(W, "l2_gather", None) else {})},
+        "e2e": {"value": algo / e2e_max / 1e9, "unit": "GB/s",
+                "h2d_bytes_per_step": W.h2d_bytes(), "d2h_bytes_per_step": W.d2h_bytes(),
+                "ms_per_step": e2e_max * 1e3},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "gen_s": W.gen_s,
+    }
+    if dist_on:
+        res["broadcast"] = {"ms": bcast_ms, "bytes": W.broadcast_bytes,
+                            "note": "shared operand broadcast once over NCCL before the steps "
+                                    "(outside the timed step)"}
+    if world == 1 and not args.no_cpu_baseline and W.cid:
+        try:
+            res["cpu_baselines"] = cpu_baselines(W, cpu_target_s)
+        except SystemExit as e:
+            res["cpu_baselines"] = {"error": str(e)}
+        except Exception as e:  # the baseline must not kill the GPU number
+            res["cpu_baselines"] = {"error": repr(e)}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=None,
+                    help="one config (1..5) as the headline; default: all five, headline 5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=0.6,
+                    help="target seconds per reference run in the cpu_baseline samples")
+    ap.add_argument("--mtx", help="SpGEMM A*A on this Matrix Market file instead of a config")
+    ap.add_argument("--tns", help="dense MTTKRP on this FROSTT .tns file instead of a config")
+    ap.add_argument("--rank", type=int, default=32, help="factor rank for --tns")
+    ap.add_argument("--mode", default="fused", choices=["fused", "assemble", "compute", "unsorted"],
+                    help="execution mode (SpGEMM / SpAdd configs): SPEC.md:372-374, sort flag :351")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    headline = args.config or HEADLINE
+    if headline not in WORKLOADS:
+        raise SystemExit(f"config {headline} not available in this build")
+    if args.impl == "reference":
+        return run_reference(args, headline)
+
+    import torch
+    import torch.distributed as dist
+
+    dist_on = "WORLD_SIZE" in os.environ and "RANK" in os.environ
+    world = int(os.environ.get("WORLD_SIZE", "1")) if dist_on else 1
+    rank = int(os.environ.get("RANK", "0")) if dist_on else 0
+    local = int(os.environ.get("LOCAL_RANK", "0")) if dist_on else 0
+    torch.cuda.set_device(local)
+    if dist_on:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1802_10574_b200 import Context
+
+    ctx = Context(local)
+    stream = torch.cuda.Stream(device=local)
+    ctx.set_stream(stream)
+
+    if args.mtx or args.tns:
+        cids = [0]
+    elif args.config:
+        cids = [args.config]
+    else:
+        cids = [c for c in (1, 2, 3, 4, 5) if c != headline] + [headline]
+    results = {}
+    for cid in cids:
+        if cid == 0:
+            W = FileSpgemmWork(args.mtx) if args.mtx else FileMttkrpWork(args.tns, args.rank)
+        else:
+            W = WORKLOADS[cid](cid, have_data=(rank == 0))
+        if args.mode != "fused":
+            if cid not in (0, 1, 2, 3) or args.tns:
+                raise SystemExit("--mode applies to the SpGEMM and SpAdd configs (1, 2, 3)")
+            W.mode = args.mode
+        results[cid] = run_config(W, args, ctx, stream, world, rank, dist_on, local,
+                                  args.cpu_seconds)
+        del W
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
     if rank == 0:
+        h = results[cids[-1]]
+        cb = h.get("cpu_baselines", {})
         line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "metric": METRIC, "value": h["value"], "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": h["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64",
-            "data": ("file " + (args.mtx or args.tns)) if W.cid == 0 else
+            "data": ("file " + (args.mtx or args.tns)) if cids[-1] == 0 else
                     "synthetic (seeded; BASELINE shapes, see DESIGN.md)",
-            "config": {"workload": W.name, "config_id": cid if W.cid else None,
-                       "l2": "inputs larger than L2 (no flush)" if flush is None
-                       else "inputs smaller than L2: 256 MB L2 flush before every timed step",
-                       "algo_bytes_per_step": algo, "nnz_out": W.nnz_out,
-                       **({"mode": W.mode} if W.mode != "fused" else {}),
-                       "parallelism": f"row shards x{world} (weak)"},
-            "useful_gflops": W.flops() * world / (ms_max * 1e-3) / 1e9,
-            "kernel_ms": kernel_ms, "kernels_total_ms": statistics.mean(tot_ms),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic(W.name, kname),
-                         "kernel": kname, "kernel_share": kernel_ms / total_kms,
-                         "kernels_per_call": launches // max(1, args.steps),
-                         "time_basis": ("device step time (the call's kernels overlap on two "
-                                        "streams; their durations sum to %.3f ms)" % total_kms)
-                         if overlapped else "sum of the call's kernel durations (CUDA events)",
-                         "peak_source": peak_src,
-                         **({"l2_gather": {"bytes_per_step": W.l2_gather,
-                                           "achieved_gbs": W.l2_gather / (basis_ms * 1e-3) / 1e9,
-                                           "note": "factor rows read per nonzero / fiber "
-                                                   "(L2-resident); the binding stream"}}
-                            if getattr(W, "l2_gather", None) else {})},
-            "e2e": {"value": algo * world / e2e_max / 1e9, "unit": "GB/s",
-                    "h2d_bytes_per_step": W.h2d_bytes(), "d2h_bytes_per_step": W.d2h_bytes(),
-                    "ms_per_step": e2e_max * 1e3},
-            "gpu_launches": launches,
-            "clocks": clk,
+            "config": {"workload": h["workload"], "config_id": h["config_id"],
+                       "l2": h["l2"], "algo_bytes_per_step": h["algo_bytes_per_step"],
+                       "nnz_out": h["nnz_out"],
+                       **({"mode": args.mode} if args.mode != "fused" else {}),
+                       "parallelism": f"row shards x{world} (strong)"},
+            "useful_gflops": h["useful_gflops"],
+            "kernel_ms": h["kernel_ms"], "kernels_total_ms": h["kernels_total_ms"],
+            "roofline": h["roofline"],
+            "e2e": h["e2e"],
+            "gpu_launches": h["gpu_launches"],
+            "clocks": h["clocks"],
         }
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                line["cpu_baseline"] = cpu_baseline(W)
-            except Exception as e:  # the baseline must not kill the GPU number
-                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        if "broadcast" in h:
+            line["broadcast"] = h["broadcast"]
+        if "all" in cb:
+            line["cpu_baseline"] = dict(cb["all"])
+            line["cpu_baseline_1thread"] = cb["1thread"]
+        elif cb:
+            line["cpu_baseline"] = {"value": None, **cb}
+        if len(cids) > 1:
+            line["configs"] = {str(c): {k: v for k, v in r.items() if k != "clocks"}
+                               for c, r in results.items()}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     ctx.close()
 

@@ -32,7 +32,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "runtime.h"
@@ -61,7 +63,17 @@ struct DenseParams {
   unsigned long long* counter;  // dynamic chunk claims
   double* part;         // [ncb][nchunks][2][32] partials (head, tail)
   int64_t* part_slice;  // [nchunks][2]: head slice (-1 none, -2 empty chunk), tail slice
+  // heavy slices (computed by mttkrp_dense_heavy_kernel; skipped by the chunked kernels)
+  int nheavy;
+  const int64_t* heavy_f;     // [nheavy][2] fiber range of each heavy slice
+  const unsigned char* heavy_flag;  // [I] 1 for a heavy slice
 };
+
+__device__ __forceinline__ bool fiber_is_heavy(const DenseParams& P, int64_t f) {
+  bool h = false;
+  for (int t = 0; t < P.nheavy; t++) h |= (f >= P.heavy_f[2 * t]) && (f < P.heavy_f[2 * t + 1]);
+  return h;
+}
 
 __device__ __forceinline__ int64_t lower_bound_g(const int64_t* a, int64_t n, int64_t x) {
   int64_t lo = 0;
@@ -172,6 +184,7 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
         t[x] += __shfl_xor_sync(kFull, t[x], 16);
         acc[x] = 0.0;
       }
+      if (P.nheavy && P.heavy_flag[st.s]) return;  // mttkrp_dense_heavy_kernel's row
       const bool started_here = !st.open;
       double* dst;
       if (started_here && ends_here) {
@@ -195,6 +208,7 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
         mj = (int)P.idx1[fg + lane];
         mz = P.pos2[fg + lane];
         mlen = (int)(P.pos2[fg + lane + 1] - mz);
+        if (P.nheavy && fiber_is_heavy(P, fg + lane)) mlen = 0;  // tiled kernel's fiber
       }
       // Steps: up to 4 consecutive short fibers, a quarter each; or one long
       // fiber (>= kLongFiber nonzeros) split over all four quarters (batch t
@@ -327,8 +341,266 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
     if (fb < st.s_end) flush(false);
     if (lane == 0) {
       if (!st.wrote_head) P.part_slice[2 * c] = -1;
-      if (!(fb < st.s_end && !st.open)) P.part_slice[2 * c + 1] = -1;
+      if (!(fb < st.s_end && !st.open) || (P.nheavy && P.heavy_flag[st.s]))
+        P.part_slice[2 * c + 1] = -1;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Heavy slices (R == 32): slices whose fibers are long enough that D rows
+// repeat many times inside a block of fibers (config 4's top slices: fibers of
+// ~3,200 / 1,100 / 600 nonzeros over K = 28,818).  Work items are blocks of
+// kHvFibers consecutive fibers of one heavy slice times a range of k.  A CTA
+// walks its item's k range in tiles of kHvTile D rows; each tile is copied
+// global -> shared by one cp.async.bulk (TMA, 48 KB contiguous: D is
+// row-major) on an mbarrier, double-buffered so the next tile lands while this
+// one is consumed.  Every quarter-warp owns 4 fibers and consumes, per tile,
+// the nonzeros whose k falls inside it, reading D from shared memory: each D
+// row is fetched from L2 once per item instead of once per nonzero (the
+// chunked kernel's 256 B per nonzero).  A fiber's w0 partial over the item's k
+// range is multiplied into C(j,:) and summed (fixed order) into the item's
+// partial row; mttkrp_dense_heavy_reduce adds an item's partials per slice in
+// item order (deterministic).
+constexpr int kHvWarps = 8;
+constexpr int kHvFibers = kHvWarps * 4 * 4;  // 8 warps x 4 quarters x 4 fibers
+#ifndef HV_TILE
+#define HV_TILE 192
+#endif
+constexpr int kHvTile = HV_TILE;  // D rows per stage (48 KB at R = 32)
+
+struct HeavyItem {
+  int64_t f0, f1;  // fibers [f0, f1), f1 - f0 <= kHvFibers, one slice
+  int32_t k0, k1;  // k range [k0, k1)
+  int32_t slot;    // heavy slice index
+  int32_t pad;
+};
+
+struct HeavySmem {
+  double tile[2][kHvTile * 32];
+  double red[kHvWarps][32];
+  uint64_t bar[2];
+  int item;
+};
+
+// Quarter-cooperative lower bound: first z in [z0, z1) with idx2[z] >= k.
+__device__ __forceinline__ int64_t quarter_lower_bound(const int64_t* idx2, int64_t z0, int64_t z1,
+                                                       int64_t k, int ql, unsigned qmask) {
+  int64_t lo = z0, hi = z1;  // answer in [lo, hi]
+  while (hi - lo > 8) {
+    const int64_t step = (hi - lo + 7) >> 3;
+    const int64_t p = lo + (int64_t)ql * step;
+    const bool lt = p < hi && idx2[p] < k;
+    const unsigned m = __ballot_sync(kFull, lt) & qmask;
+    const int nlt = __popc(m);  // samples below k (a prefix: idx2 sorted)
+    if (nlt == 0) {
+      hi = lo;
+      break;
+    }
+    lo = lo + (int64_t)(nlt - 1) * step + 1;
+    hi = min(hi, lo - 1 + step);
+  }
+  // final linear pass over <= 8 candidates
+  const int64_t p = lo + ql;
+  const bool lt = p < hi && idx2[p] < k;
+  return lo + __popc(__ballot_sync(kFull, lt) & qmask);
+}
+
+__global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
+    const DenseParams P, const HeavyItem* items, int nitems, unsigned long long* claim,
+    double* hpart) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  HeavySmem& S = *reinterpret_cast<HeavySmem*>(smem_raw);
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int q = lane >> 3, ql = lane & 7;
+  const int qbase = lane & ~7;
+  const unsigned qmask = 0xffu << qbase;
+  // lane columns: 2ql, 2ql+1 and 16+2ql, 16+2ql+1 (a quarter's 16-byte loads
+  // of one row are contiguous: conflict-free shared reads)
+  const int ca = 2 * ql, cb = 16 + 2 * ql;
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t gt = 0;  // tiles consumed by this CTA (stage = gt & 1, parity = (gt >> 1) & 1)
+  auto issue = [&](const HeavyItem& it, int t, uint32_t g) {
+    const int kt0 = it.k0 + t * kHvTile;
+    const int rows = min(kHvTile, it.k1 - kt0);
+    const uint32_t bytes = (uint32_t)rows * 256u;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&S.bar[g & 1], bytes);
+    bulk_g2s(S.tile[g & 1], P.D + (int64_t)kt0 * 32, bytes, &S.bar[g & 1]);
+  };
+  while (true) {
+    if (threadIdx.x == 0) S.item = (int)atomicAdd(claim, 1ull);
+    __syncthreads();
+    const int itn = S.item;
+    if (itn >= nitems) break;
+    const HeavyItem it = items[itn];
+    const int nt = (it.k1 - it.k0 + kHvTile - 1) / kHvTile;
+    if (threadIdx.x == 0) {
+      issue(it, 0, gt);
+      if (nt > 1) issue(it, 1, gt + 1);
+    }
+    // this quarter's 4 fibers: current batch of 8 nonzeros (lane ql holds
+    // entry cur + ql) and the next batch, prefetched
+    int64_t cur[4], zend[4];
+    int used[4];
+    int kb[4], kn[4];
+    double bb[4], bn[4];
+    double w[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t f = it.f0 + warp * 16 + q * 4 + u;
+      int64_t z0 = 0, z1 = 0;
+      if (f < it.f1) {
+        z0 = P.pos2[f];
+        z1 = P.pos2[f + 1];
+      }
+      if (it.k0 > 0) z0 = quarter_lower_bound(P.idx2, z0, z1, it.k0, ql, qmask);
+      cur[u] = z0;
+      zend[u] = z1;
+      used[u] = 0;
+      const int64_t za = z0 + ql, zb = z0 + 8 + ql;
+      kb[u] = za < z1 ? (int)P.idx2[za] : INT_MAX;
+      bb[u] = za < z1 ? P.vals[za] : 0.0;
+      kn[u] = zb < z1 ? (int)P.idx2[zb] : INT_MAX;
+      bn[u] = zb < z1 ? P.vals[zb] : 0.0;
+#pragma unroll
+      for (int x = 0; x < 4; x++) w[u][x] = 0.0;
+    }
+    for (int t = 0; t < nt; t++, gt++) {
+      const int kt0 = it.k0 + t * kHvTile;
+      const int kt1 = min(it.k1, kt0 + kHvTile);
+      mbar_wait_parity(&S.bar[gt & 1], (gt >> 1) & 1);
+      const double* tile = S.tile[gt & 1];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        while (true) {
+          // entries [used, 8) of the batch with k < kt1 (a prefix: k sorted)
+          const bool in = ql >= used[u] && kb[u] < kt1;
+          const unsigned m = (__ballot_sync(kFull, in) & qmask) >> qbase;
+          const int n = __popc(m);
+          const int nmax = __reduce_max_sync(kFull, (unsigned)n);
+          if (nmax == 0) break;  // uniform
+          for (int e0 = 0; e0 < nmax; e0 += 4) {
+            double2 da[4], db[4];
+            double b[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+              const int e = e0 + v;
+              const int src = qbase + min(7, used[u] + e);
+              const int k = __shfl_sync(kFull, kb[u], src);
+              const double bv = __shfl_sync(kFull, bb[u], src);
+              const bool ok = e < n;
+              b[v] = ok ? bv : 0.0;
+              const double* row = tile + (ok ? (k - kt0) : 0) * 32;
+              da[v] = *reinterpret_cast<const double2*>(row + ca);
+              db[v] = *reinterpret_cast<const double2*>(row + cb);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+              w[u][0] = fma(b[v], da[v].x, w[u][0]);
+              w[u][1] = fma(b[v], da[v].y, w[u][1]);
+              w[u][2] = fma(b[v], db[v].x, w[u][2]);
+              w[u][3] = fma(b[v], db[v].y, w[u][3]);
+            }
+          }
+          used[u] += n;
+          // a fully consumed batch: the prefetched one becomes current
+          const bool adv = used[u] == 8;
+          if (adv) {
+            cur[u] += 8;
+            used[u] = 0;
+            kb[u] = kn[u];
+            bb[u] = bn[u];
+            const int64_t zb = cur[u] + 8 + ql;
+            kn[u] = zb < zend[u] ? (int)P.idx2[zb] : INT_MAX;
+            bn[u] = zb < zend[u] ? P.vals[zb] : 0.0;
+          }
+          if (!__any_sync(kFull, adv)) break;
+        }
+      }
+      __syncthreads();  // every warp is done with this stage
+      if (threadIdx.x == 0 && t + 2 < nt) issue(it, t + 2, gt + 2);
+    }
+    // w0 (partial over [k0, k1)) x C(j,:), summed over the quarter's fibers,
+    // the warp's quarters and the CTA's warps in a fixed order
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t f = it.f0 + warp * 16 + q * 4 + u;
+      if (f < it.f1) {
+        const int64_t j = P.idx1[f];
+        const double2 c0 = __ldg(reinterpret_cast<const double2*>(P.C + j * 32 + ca));
+        const double2 c1 = __ldg(reinterpret_cast<const double2*>(P.C + j * 32 + cb));
+        acc[0] = fma(w[u][0], c0.x, acc[0]);
+        acc[1] = fma(w[u][1], c0.y, acc[1]);
+        acc[2] = fma(w[u][2], c1.x, acc[2]);
+        acc[3] = fma(w[u][3], c1.y, acc[3]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; x++) {
+      acc[x] += __shfl_xor_sync(kFull, acc[x], 8);
+      acc[x] += __shfl_xor_sync(kFull, acc[x], 16);
+    }
+    if (q == 0) {
+      S.red[warp][ca] = acc[0];
+      S.red[warp][ca + 1] = acc[1];
+      S.red[warp][cb] = acc[2];
+      S.red[warp][cb + 1] = acc[3];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double sum = 0.0;
+#pragma unroll
+      for (int x = 0; x < kHvWarps; x++) sum += S.red[x][lane];
+      hpart[(int64_t)itn * 32 + lane] = sum;
+    }
+  }
+}
+
+// Heavy slice rows: a warp per slice adds its items' partial rows in item order.
+__global__ void mttkrp_dense_heavy_reduce_kernel(const DenseParams P, const HeavyItem* items,
+                                                 int nitems, const double* hpart,
+                                                 const int64_t* heavy_s) {
+  const int lane = (int)lane_id();
+  const int hs = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (hs >= P.nheavy) return;
+  double sum = 0.0;
+  for (int t = 0; t < nitems; t++)
+    if (items[t].slot == hs) sum += hpart[(int64_t)t * 32 + lane];
+  P.A[heavy_s[hs] * 32 + lane] = sum;
+}
+
+// Per-slice nnz and fibers; slices whose average fiber is long enough for a
+// block of kHvFibers fibers to reuse each staged D row (avg length > 2K /
+// kHvFibers) and that hold at least one full block are listed as heavy.
+constexpr int kMaxHeavy = 64;
+__global__ void mttkrp_dense_heavy_select_kernel(const DenseParams P, int64_t min_len,
+                                                 unsigned char* flag, int64_t* list,
+                                                 unsigned long long* count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.I;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
+    const int64_t nz = f1 > f0 ? P.pos2[f1] - P.pos2[f0] : 0;
+    bool heavy = f1 - f0 >= kHvFibers && nz >= min_len * (f1 - f0);
+    if (heavy) {
+      const unsigned long long at = atomicAdd(count, 1ull);
+      if (at < kMaxHeavy) {
+        list[4 * at] = i;
+        list[4 * at + 1] = f0;
+        list[4 * at + 2] = f1;
+        list[4 * at + 3] = nz;
+      } else {
+        heavy = false;
+      }
+    }
+    flag[i] = heavy ? 1 : 0;
   }
 }
 
@@ -979,6 +1251,86 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       call.before_launch("mttkrp_dense_bounds");
       mttkrp_dense_bounds_kernel<<<(unsigned)ceil_div(P.nchunks + 1, 256), 256, 0, call.stream()>>>(P);
       call.after_launch();
+      // heavy slices -> the TMA-tiled kernel (beside the chunked one)
+      const bool a16 = ((uintptr_t)P.D % 16 == 0);
+      std::vector<HeavyItem> items;
+      int64_t* heavy_s = nullptr;
+      double* hpart = nullptr;
+      HeavyItem* d_items = nullptr;
+#ifndef HV_DISABLE
+      if (fast && a16 && P.K >= 4 * kHvTile) {
+        auto* hflag = static_cast<unsigned char*>(call.scratch((size_t)I));
+        auto* hlist = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * (4 * kMaxHeavy + 1)));
+        auto* hcount = reinterpret_cast<unsigned long long*>(hlist + 4 * kMaxHeavy);
+        const int64_t min_len = std::max<int64_t>(64, ceil_div(2 * P.K, (int64_t)kHvFibers));
+        call.before_launch("mttkrp_dense_heavy_select");
+        mttkrp_dense_heavy_select_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 256), (int64_t)sms * 8),
+                                           256, 0, call.stream()>>>(P, min_len, hflag, hlist, hcount);
+        call.after_launch();
+        int64_t hl[4 * kMaxHeavy + 1];
+        call.read_scalars(hlist, 4 * kMaxHeavy + 1, hl);
+        const int nh = (int)std::min<int64_t>(hl[4 * kMaxHeavy], kMaxHeavy);
+        if (nh > 0) {
+          // heaviest first; fiber blocks of kHvFibers, each split over k so an
+          // item holds ~1/4 of a fair share of the heavy nonzeros per CTA slot
+          std::vector<int> order(nh);
+          for (int h = 0; h < nh; h++) order[h] = h;
+          std::sort(order.begin(), order.end(), [&](int a, int b) { return hl[4 * a + 3] > hl[4 * b + 3]; });
+          int64_t hnz = 0;
+          for (int h = 0; h < nh; h++) hnz += hl[4 * h + 3];
+          const int64_t target = std::max<int64_t>(16384, hnz / ((int64_t)sms * 2 * 4));
+          std::vector<int64_t> hs(nh), hf(2 * nh);
+          const int64_t ktiles = ceil_div(P.K, (int64_t)kHvTile);
+          for (int o = 0; o < nh; o++) {
+            const int h = order[o];
+            hs[o] = hl[4 * h];
+            hf[2 * o] = hl[4 * h + 1];
+            hf[2 * o + 1] = hl[4 * h + 2];
+            const int64_t nf = hf[2 * o + 1] - hf[2 * o];
+            const double per_fiber = (double)hl[4 * h + 3] / (double)nf;
+            for (int64_t b0 = hf[2 * o]; b0 < hf[2 * o + 1]; b0 += kHvFibers) {
+              const int64_t b1 = std::min<int64_t>(hf[2 * o + 1], b0 + kHvFibers);
+              const int64_t est = (int64_t)(per_fiber * (double)(b1 - b0));
+              const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(ktiles, (est + target / 2) / target));
+              for (int64_t p = 0; p < ks; p++) {
+                HeavyItem itm{};
+                itm.f0 = b0;
+                itm.f1 = b1;
+                itm.k0 = (int32_t)std::min<int64_t>(P.K, ktiles * p / ks * kHvTile);
+                itm.k1 = (int32_t)std::min<int64_t>(P.K, ktiles * (p + 1) / ks * kHvTile);
+                itm.slot = o;
+                if (itm.k1 > itm.k0) items.push_back(itm);
+              }
+            }
+          }
+          P.nheavy = nh;
+          P.heavy_flag = hflag;
+          auto* d_hf = call.scratch_n<int64_t>((size_t)(2 * nh));
+          heavy_s = call.scratch_n<int64_t>((size_t)nh);
+          d_items = call.scratch_n<HeavyItem>(items.size());
+          hpart = call.scratch_n<double>(items.size() * 32);
+          STAM_CUDA_CHECK(cudaMemcpyAsync(d_hf, hf.data(), sizeof(int64_t) * hf.size(),
+                                          cudaMemcpyHostToDevice, call.stream()));
+          STAM_CUDA_CHECK(cudaMemcpyAsync(heavy_s, hs.data(), sizeof(int64_t) * hs.size(),
+                                          cudaMemcpyHostToDevice, call.stream()));
+          STAM_CUDA_CHECK(cudaMemcpyAsync(d_items, items.data(), sizeof(HeavyItem) * items.size(),
+                                          cudaMemcpyHostToDevice, call.stream()));
+          P.heavy_f = d_hf;
+          // the host vectors must outlive the async copies
+          STAM_CUDA_CHECK(cudaStreamSynchronize(call.stream()));
+          auto* hclaim = static_cast<unsigned long long*>(call.scratch_zero(16));
+          cudaStream_t aux = call.fork();
+          const size_t hsm = sizeof(HeavySmem);
+          STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_dense_heavy_kernel,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+          call.before_launch("mttkrp_dense_heavy", aux);
+          mttkrp_dense_heavy_kernel<<<(unsigned)std::min<int64_t>((int64_t)items.size(), (int64_t)sms * 2),
+                                      kHvWarps * 32, hsm, aux>>>(P, d_items, (int)items.size(), hclaim,
+                                                                hpart);
+          call.after_launch(aux);
+        }
+      }
+#endif
       call.before_launch(fast ? "mttkrp_dense32" : "mttkrp_dense_generic");
       if (fast)
       {
@@ -1014,6 +1366,14 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       mttkrp_dense_fixup_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(P.nchunks, 8), (int64_t)sms * 8)),
                                   256, 0, call.stream()>>>(P, L);
       call.after_launch();
+      if (P.nheavy > 0) {
+        call.join();
+        call.before_launch("mttkrp_dense_heavy_reduce");
+        mttkrp_dense_heavy_reduce_kernel<<<(unsigned)ceil_div((int64_t)P.nheavy * 32, 256), 256, 0,
+                                           call.stream()>>>(P, d_items, (int)items.size(), hpart,
+                                                            heavy_s);
+        call.after_launch();
+      }
     }
     call.finish_dense_result(A);
     call.finish();

@@ -62,7 +62,8 @@ def _worker(rank, world, port, q):
             return CSR(out["nrows"], out["ncols"], out["pos"], out["idx"], out["vals"])
 
         A = cfg["A"] if cfg else None
-        r0, C = S.distributed_spgemm(A, A, compute, gather=True)
+        r0, C = S.distributed_spgemm(A, A, lambda a, b: compute(a.numpy(), b.numpy()),
+                                     gather=True, same=True)
         if rank == 0:
             ref = oracle.spgemm(cfg["A"], cfg["A"])
             ok = (np.array_equal(C.pos, ref["pos"]) and np.array_equal(C.idx, ref["idx"])
@@ -105,7 +106,7 @@ def _worker_more(rank, world, port, q):
             return CSR(o["nrows"], o["ncols"], o["pos"], o["idx"], o["vals"])
 
         c2 = G.make_config(2, scale=0.002) if rank == 0 else None
-        _, D = S.distributed_spadd(c2["ops"] if c2 else None, lambda ops: as_csr(oracle.spadd(ops)),
+        _, D = S.distributed_spadd(c2["ops"] if c2 else None, lambda ops: as_csr(oracle.spadd([o.numpy() for o in ops])),
                                    gather=True)
         c4 = G.make_config(4, scale=0.003) if rank == 0 else None
         A4 = S.distributed_mttkrp_dense(
