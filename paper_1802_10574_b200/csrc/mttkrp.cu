@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,12 @@
 
 namespace stamgpu {
 namespace {
+
+// Runtime switch for A/B measurements of alternative paths (default on).
+inline bool env_flag(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) != 0 : dflt != 0;
+}
 
 // ===========================================================================
 // dense
@@ -362,8 +369,13 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
 // range is multiplied into C(j,:) and summed (fixed order) into the item's
 // partial row; mttkrp_dense_heavy_reduce adds an item's partials per slice in
 // item order (deterministic).
-constexpr int kHvWarps = 8;
-constexpr int kHvFibers = kHvWarps * 4 * 4;  // 8 warps x 4 quarters x 4 fibers
+#ifndef HV_FPQ
+#define HV_FPQ 2
+#endif
+constexpr int kHvWarps = 16;
+constexpr int kHvFpq = HV_FPQ;                      // fibers per quarter-warp
+constexpr int kHvFibers = kHvWarps * 4 * kHvFpq;   // fibers per work item
+constexpr int kHvDepth = 3;                          // batches of 8 nonzeros held per fiber
 #ifndef HV_TILE
 #define HV_TILE 192
 #endif
@@ -384,29 +396,33 @@ struct HeavySmem {
 };
 
 // Quarter-cooperative lower bound: first z in [z0, z1) with idx2[z] >= k.
+// Every quarter of the warp searches its own range; the loop runs while any
+// quarter is still narrowing (ballots are warp-wide).
 __device__ __forceinline__ int64_t quarter_lower_bound(const int64_t* idx2, int64_t z0, int64_t z1,
                                                        int64_t k, int ql, unsigned qmask) {
   int64_t lo = z0, hi = z1;  // answer in [lo, hi]
-  while (hi - lo > 8) {
-    const int64_t step = (hi - lo + 7) >> 3;
+  while (__any_sync(kFull, hi - lo > 8)) {
+    const bool act = hi - lo > 8;  // uniform within the quarter
+    const int64_t step = act ? (hi - lo + 7) >> 3 : 0;
     const int64_t p = lo + (int64_t)ql * step;
-    const bool lt = p < hi && idx2[p] < k;
-    const unsigned m = __ballot_sync(kFull, lt) & qmask;
-    const int nlt = __popc(m);  // samples below k (a prefix: idx2 sorted)
-    if (nlt == 0) {
-      hi = lo;
-      break;
+    const bool lt = act && p < hi && idx2[p] < k;
+    const int nlt = __popc(__ballot_sync(kFull, lt) & qmask);  // samples below k: a prefix
+    if (act) {
+      if (nlt == 0) {
+        hi = lo;
+      } else {
+        lo = lo + (int64_t)(nlt - 1) * step + 1;
+        hi = min(hi, lo - 1 + step);
+      }
     }
-    lo = lo + (int64_t)(nlt - 1) * step + 1;
-    hi = min(hi, lo - 1 + step);
   }
-  // final linear pass over <= 8 candidates
+  // final pass over <= 8 candidates
   const int64_t p = lo + ql;
   const bool lt = p < hi && idx2[p] < k;
   return lo + __popc(__ballot_sync(kFull, lt) & qmask);
 }
 
-__global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
+__global__ void __launch_bounds__(kHvWarps * 32, 1) mttkrp_dense_heavy_kernel(
     const DenseParams P, const HeavyItem* items, int nitems, unsigned long long* claim,
     double* hpart) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -445,16 +461,17 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
       issue(it, 0, gt);
       if (nt > 1) issue(it, 1, gt + 1);
     }
-    // this quarter's 4 fibers: current batch of 8 nonzeros (lane ql holds
-    // entry cur + ql) and the next batch, prefetched
-    int64_t cur[4], zend[4];
-    int used[4];
-    int kb[4], kn[4];
-    double bb[4], bn[4];
-    double w[4][4];
+    // this quarter's fibers: kHvDepth batches of 8 nonzeros in flight (lane ql
+    // holds entry cur + 8d + ql of batch d); batch 0 is being consumed
+    int64_t cur[kHvFpq];
+    int32_t zrem[kHvFpq];  // entries from cur to the fiber's end
+    int used[kHvFpq];
+    int kb[kHvFpq][kHvDepth];
+    double bb[kHvFpq][kHvDepth];
+    double w[kHvFpq][4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int64_t f = it.f0 + warp * 16 + q * 4 + u;
+    for (int u = 0; u < kHvFpq; u++) {
+      const int64_t f = it.f0 + (warp * 4 + q) * kHvFpq + u;
       int64_t z0 = 0, z1 = 0;
       if (f < it.f1) {
         z0 = P.pos2[f];
@@ -462,13 +479,14 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
       }
       if (it.k0 > 0) z0 = quarter_lower_bound(P.idx2, z0, z1, it.k0, ql, qmask);
       cur[u] = z0;
-      zend[u] = z1;
+      zrem[u] = (int32_t)(z1 - z0);
       used[u] = 0;
-      const int64_t za = z0 + ql, zb = z0 + 8 + ql;
-      kb[u] = za < z1 ? (int)P.idx2[za] : INT_MAX;
-      bb[u] = za < z1 ? P.vals[za] : 0.0;
-      kn[u] = zb < z1 ? (int)P.idx2[zb] : INT_MAX;
-      bn[u] = zb < z1 ? P.vals[zb] : 0.0;
+#pragma unroll
+      for (int d = 0; d < kHvDepth; d++) {
+        const int e = 8 * d + ql;
+        kb[u][d] = e < zrem[u] ? (int)P.idx2[z0 + e] : INT_MAX;
+        bb[u][d] = e < zrem[u] ? P.vals[z0 + e] : 0.0;
+      }
 #pragma unroll
       for (int x = 0; x < 4; x++) w[u][x] = 0.0;
     }
@@ -478,10 +496,10 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
       mbar_wait_parity(&S.bar[gt & 1], (gt >> 1) & 1);
       const double* tile = S.tile[gt & 1];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < kHvFpq; u++) {
         while (true) {
-          // entries [used, 8) of the batch with k < kt1 (a prefix: k sorted)
-          const bool in = ql >= used[u] && kb[u] < kt1;
+          // entries [used, 8) of batch 0 with k < kt1 (a prefix: k sorted)
+          const bool in = ql >= used[u] && kb[u][0] < kt1;
           const unsigned m = (__ballot_sync(kFull, in) & qmask) >> qbase;
           const int n = __popc(m);
           const int nmax = __reduce_max_sync(kFull, (unsigned)n);
@@ -493,8 +511,8 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
             for (int v = 0; v < 4; v++) {
               const int e = e0 + v;
               const int src = qbase + min(7, used[u] + e);
-              const int k = __shfl_sync(kFull, kb[u], src);
-              const double bv = __shfl_sync(kFull, bb[u], src);
+              const int k = __shfl_sync(kFull, kb[u][0], src);
+              const double bv = __shfl_sync(kFull, bb[u][0], src);
               const bool ok = e < n;
               b[v] = ok ? bv : 0.0;
               const double* row = tile + (ok ? (k - kt0) : 0) * 32;
@@ -510,16 +528,20 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
             }
           }
           used[u] += n;
-          // a fully consumed batch: the prefetched one becomes current
+          // a fully consumed batch: shift the ring, prefetch kHvDepth batches ahead
           const bool adv = used[u] == 8;
           if (adv) {
             cur[u] += 8;
+            zrem[u] -= 8;
             used[u] = 0;
-            kb[u] = kn[u];
-            bb[u] = bn[u];
-            const int64_t zb = cur[u] + 8 + ql;
-            kn[u] = zb < zend[u] ? (int)P.idx2[zb] : INT_MAX;
-            bn[u] = zb < zend[u] ? P.vals[zb] : 0.0;
+#pragma unroll
+            for (int d = 0; d + 1 < kHvDepth; d++) {
+              kb[u][d] = kb[u][d + 1];
+              bb[u][d] = bb[u][d + 1];
+            }
+            const int e = 8 * (kHvDepth - 1) + ql;
+            kb[u][kHvDepth - 1] = e < zrem[u] ? (int)P.idx2[cur[u] + e] : INT_MAX;
+            bb[u][kHvDepth - 1] = e < zrem[u] ? P.vals[cur[u] + e] : 0.0;
           }
           if (!__any_sync(kFull, adv)) break;
         }
@@ -531,8 +553,8 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
     // the warp's quarters and the CTA's warps in a fixed order
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int64_t f = it.f0 + warp * 16 + q * 4 + u;
+    for (int u = 0; u < kHvFpq; u++) {
+      const int64_t f = it.f0 + (warp * 4 + q) * kHvFpq + u;
       if (f < it.f1) {
         const int64_t j = P.idx1[f];
         const double2 c0 = __ldg(reinterpret_cast<const double2*>(P.C + j * 32 + ca));
@@ -564,17 +586,24 @@ __global__ void __launch_bounds__(kHvWarps * 32, 2) mttkrp_dense_heavy_kernel(
   }
 }
 
-// Heavy slice rows: a warp per slice adds its items' partial rows in item order.
-__global__ void mttkrp_dense_heavy_reduce_kernel(const DenseParams P, const HeavyItem* items,
-                                                 int nitems, const double* hpart,
-                                                 const int64_t* heavy_s) {
+// Heavy slice rows: a CTA per slice; warp w adds the slice's items w, w+32,
+// ... in order, then warp 0 adds the 32 warp sums in order (deterministic).
+__global__ void mttkrp_dense_heavy_reduce_kernel(const DenseParams P, const int* slot_items,
+                                                 const double* hpart, const int64_t* heavy_s) {
+  __shared__ double ws[32][33];
   const int lane = (int)lane_id();
-  const int hs = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (hs >= P.nheavy) return;
+  const int warp = threadIdx.x >> 5;
+  const int hs = blockIdx.x;
+  const int t0 = slot_items[hs], t1 = slot_items[hs + 1];
   double sum = 0.0;
-  for (int t = 0; t < nitems; t++)
-    if (items[t].slot == hs) sum += hpart[(int64_t)t * 32 + lane];
-  P.A[heavy_s[hs] * 32 + lane] = sum;
+  for (int t = t0 + warp; t < t1; t += 32) sum += hpart[(int64_t)t * 32 + lane];
+  ws[warp][lane] = sum;
+  __syncthreads();
+  if (warp == 0) {
+    double tot = 0.0;
+    for (int x = 0; x < 32; x++) tot += ws[x][lane];
+    P.A[heavy_s[hs] * 32 + lane] = tot;
+  }
 }
 
 // Per-slice nnz and fibers; slices whose average fiber is long enough for a
@@ -972,6 +1001,21 @@ __device__ __forceinline__ void load_bm(const unsigned long long* p, unsigned lo
   }
 }
 
+// load_bm with the L2 evict_last hint (the bitmaps are re-read ~400 times per
+// call while the CSF streams past them once).
+template <int W>
+__device__ __forceinline__ void load_bm_keep(const unsigned long long* p, uint64_t pol,
+                                             unsigned long long (&b)[W]) {
+  if constexpr (W % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < W; k += 4) ld_keep_v4(p + k, pol, b[k], b[k + 1], b[k + 2], b[k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; k++)
+      b[k] = (unsigned long long)ld_keep(reinterpret_cast<const int64_t*>(p) + k, pol);
+  }
+}
+
 // Position of column r among the row's columns (popcount of the bits below).
 template <int W>
 __device__ __forceinline__ int bm_rank(const unsigned long long (&b)[W], int r) {
@@ -985,35 +1029,34 @@ __device__ __forceinline__ int bm_rank(const unsigned long long (&b)[W], int r) 
   return n;
 }
 
-// Matches (C_j ∩ D_k columns of single-nonzero fibers) queued per warp so
-// that their value gathers and workspace updates run on full warps instead
-// of the few lanes that found a match.
-constexpr int kQ = 128;
-struct MatchQueue {
-  int64_t ci[kQ];  // position of C(j,r) in C's values
-  int64_t di[kQ];  // position of D(k,r) in D's values
-  double b[kQ];    // B(i,j,k)
-  int r[kQ];
+// Matches (C_j ∩ D_k columns of single-nonzero fibers) are expanded warp-
+// cooperatively: every lane with matches parks its fiber's (C row start, D
+// row start, b, match / C / D bitmaps) in a per-warp shared buffer, then the
+// warp's matches are numbered (a warp scan) and taken 32 at a time, lane s
+// evaluating match s: owner lane by a shuffle search over the scan, the
+// owner's t-th matched column by popcounts over its bitmap, the value
+// positions by popcounts of the C and D bitmaps below it.  No per-lane bit
+// walk (a lane with two matches no longer holds 31 others back).
+template <int W>
+struct MatchOwners {
+  int64_t c0[32];
+  int64_t d0[32];
+  double b[32];
+  unsigned long long m[W][32];
+  unsigned long long bc[W][32];
+  unsigned long long bd[W][32];
 };
+__host__ __device__ constexpr size_t match_owners_bytes(int W) { return (size_t)(3 + 3 * W) * 32 * 8; }
 
 // sparse_slice with factor-row bitmaps: C_j ∩ D_k is a word-wise AND and a
-// matched column's value positions are popcounts; matches are queued and
-// evaluated 32 at a time (same arithmetic and per-entry order as
-// sparse_slice: w0 = 0 + b*D(k,r), w1(r) += w0*C(j,r)).
+// matched column's value positions are popcounts (same arithmetic and
+// per-entry order as sparse_slice: w0 = 0 + b*D(k,r), w1(r) += w0*C(j,r)).
 template <int W>
 __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, uint32_t* wb,
-                                unsigned long long& mults, MatchQueue& Q) {
+                                unsigned long long& mults, MatchOwners<W>& O) {
   const int lane = (int)lane_id();
   const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
-  int qn = 0;  // queued matches (warp-uniform)
-  auto flush = [&]() {
-    for (int t = lane; t < qn; t += 32) {
-      const double w0 = add_rn(0.0, mul_rn(Q.b[t], P.dvals[Q.di[t]]));
-      ws_add(wv, wb, Q.r[t], mul_rn(w0, P.cvals[Q.ci[t]]));
-    }
-    __syncwarp();
-    qn = 0;
-  };
+  const uint64_t keep = l2_evict_last_policy();
   for (int64_t fb = f0; fb < f1; fb += 32) {
     const int64_t f = fb + lane;
     int nm = 0;
@@ -1025,14 +1068,14 @@ __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, ui
     for (int w = 0; w < W; w++) m[w] = bc[w] = bd[w] = 0ull;
     bool single = false;
     if (f < f1) {
-      j = P.idx1[f];
-      const int64_t z0 = P.pos2[f], z1 = P.pos2[f + 1];
-      load_bm<W>(P.cbm + j * W, bc);
+      j = __ldcs(P.idx1 + f);
+      const int64_t z0 = __ldcs(P.pos2 + f), z1 = __ldcs(P.pos2 + f + 1);
+      load_bm_keep<W>(P.cbm + j * W, keep, bc);
       if (z1 - z0 == 1) {
         single = true;
-        k = P.idx2[z0];
-        b = P.vals[z0];
-        load_bm<W>(P.dbm + k * W, bd);
+        k = __ldcs(P.idx2 + z0);
+        b = __ldcs(P.vals + z0);
+        load_bm_keep<W>(P.dbm + k * W, keep, bd);
 #pragma unroll
         for (int w = 0; w < W; w++) {
           mults += (unsigned long long)__popcll(bd[w]);
@@ -1079,44 +1122,61 @@ __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, ui
     const int inc = warp_inclusive_scan(nm);
     const int tot = __shfl_sync(kFull, inc, 31);
     if (tot == 0) continue;
-    if (tot > kQ - qn) flush();
-    const bool direct = tot > kQ;  // more matches than the queue holds: per lane
-    if (single && nm > 0) {
-      const int64_t c0 = P.cpos[j], d0 = P.dpos[k];
-      int slot = qn + inc - nm;
-      int rc = 0, rd = 0;
+    if (nm > 0) {
+      O.c0[lane] = ld_keep(P.cpos + j, keep);
+      O.d0[lane] = ld_keep(P.dpos + k, keep);
+      O.b[lane] = b;
 #pragma unroll
       for (int w = 0; w < W; w++) {
-        unsigned long long mm = m[w];
-        while (mm) {
-          const int bit = __ffsll((long long)mm) - 1;
-          const unsigned long long below = (1ull << bit) - 1ull;
-          const int64_t ci = c0 + rc + __popcll(bc[w] & below);
-          const int64_t di = d0 + rd + __popcll(bd[w] & below);
-          if (direct) {
-            const double w0 = add_rn(0.0, mul_rn(b, P.dvals[di]));
-            ws_add(wv, wb, w * 64 + bit, mul_rn(w0, P.cvals[ci]));
-          } else {
-            Q.ci[slot] = ci;
-            Q.di[slot] = di;
-            Q.b[slot] = b;
-            Q.r[slot] = w * 64 + bit;
-            slot++;
-          }
-          mults++;
-          mm &= mm - 1ull;
-        }
-        rc += __popcll(bc[w]);
-        rd += __popcll(bd[w]);
+        O.m[w][lane] = m[w];
+        O.bc[w][lane] = bc[w];
+        O.bd[w][lane] = bd[w];
       }
     }
     __syncwarp();
-    if (!direct) {
-      qn += tot;
-      if (qn >= kQ - 32) flush();
+    mults += (unsigned long long)nm;
+    for (int g0 = 0; g0 < tot; g0 += 32) {  // warp-uniform
+      const int g = g0 + lane;
+      // owner: the lowest lane whose inclusive count exceeds g
+      int o = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int iv = __shfl_sync(kFull, inc, (o + st - 1) & 31);
+        if (iv <= g) o += st;
+      }
+      const int ex = __shfl_sync(kFull, inc, o) - __shfl_sync(kFull, nm, o);
+      if (g < tot) {
+        int t = g - ex;  // the owner's t-th match
+        int r = 0, below_c = 0, below_d = 0;
+        bool found = false;
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          const unsigned long long mw = O.m[w][o];
+          const unsigned long long cw = O.bc[w][o], dw = O.bd[w][o];
+          const int pc = __popcll(mw);
+          if (!found && t < pc) {
+            // t-th set bit of mw (32-bit halves: __fns)
+            const unsigned lo = (unsigned)mw;
+            const int plo = __popc(lo);
+            const int bit = t < plo ? (int)__fns(lo, 0, t + 1)
+                                    : 32 + (int)__fns((unsigned)(mw >> 32), 0, t - plo + 1);
+            const unsigned long long bl = (1ull << bit) - 1ull;
+            r = w * 64 + bit;
+            below_c += __popcll(cw & bl);
+            below_d += __popcll(dw & bl);
+            found = true;
+          } else if (!found) {
+            t -= pc;
+            below_c += __popcll(cw);
+            below_d += __popcll(dw);
+          }
+        }
+        const double w0 = add_rn(0.0, mul_rn(O.b[o], ld_keep(P.dvals + O.d0[o] + below_d, keep)));
+        ws_add(wv, wb, r, mul_rn(w0, ld_keep(P.cvals + O.c0[o] + below_c, keep)));
+      }
     }
+    __syncwarp();  // the owner buffer is rewritten by the next batch
   }
-  flush();
 }
 
 // Each warp claims slices dynamically, evaluates one into its shared-memory
@@ -1137,7 +1197,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
   const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
   double* wv = reinterpret_cast<double*>(smem_raw + (size_t)warp * ws_bytes);
   uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
-  MatchQueue* queues = reinterpret_cast<MatchQueue*>(smem_raw + (size_t)kSpWarps * ws_bytes);
+  auto* owners = reinterpret_cast<MatchOwners<(W > 0 ? W : 1)>*>(
+      smem_raw + (size_t)kSpWarps * ws_bytes + (size_t)warp * match_owners_bytes(W > 0 ? W : 1));
   unsigned long long mults = 0;
   while (true) {
     int64_t i = 0;
@@ -1148,7 +1209,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
     for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
     __syncwarp();
     if constexpr (W > 0)
-      sparse_slice_bm<W>(P, i, wv, wb, mults, queues[warp]);
+      sparse_slice_bm<W>(P, i, wv, wb, mults, *owners);
     else
       sparse_slice(P, i, wv, wb, mults);
     __syncwarp();
@@ -1162,8 +1223,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
       if ((bits >> lane) & 1u) {
         const int rank = __popc(bits & ((1u << lane) - 1u));
         const int64_t r = (int64_t)w * 32 + lane;
-        oi[out + rank] = r;
-        ov[out + rank] = wv[r];
+        __stcs(reinterpret_cast<long long*>(oi) + out + rank, (long long)r);
+        __stcs(ov + out + rank, wv[r]);
       }
       out += __popc(bits);
     }
@@ -1257,8 +1318,9 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       int64_t* heavy_s = nullptr;
       double* hpart = nullptr;
       HeavyItem* d_items = nullptr;
+      int* slot_items = nullptr;
 #ifndef HV_DISABLE
-      if (fast && a16 && P.K >= 4 * kHvTile) {
+      if (fast && a16 && P.K >= 4 * kHvTile && env_flag("STAM_HV", 1)) {
         auto* hflag = static_cast<unsigned char*>(call.scratch((size_t)I));
         auto* hlist = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * (4 * kMaxHeavy + 1)));
         auto* hcount = reinterpret_cast<unsigned long long*>(hlist + 4 * kMaxHeavy);
@@ -1278,7 +1340,7 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
           std::sort(order.begin(), order.end(), [&](int a, int b) { return hl[4 * a + 3] > hl[4 * b + 3]; });
           int64_t hnz = 0;
           for (int h = 0; h < nh; h++) hnz += hl[4 * h + 3];
-          const int64_t target = std::max<int64_t>(16384, hnz / ((int64_t)sms * 2 * 4));
+          const int64_t target = std::max<int64_t>(16384, hnz / ((int64_t)sms * 4));
           std::vector<int64_t> hs(nh), hf(2 * nh);
           const int64_t ktiles = ceil_div(P.K, (int64_t)kHvTile);
           for (int o = 0; o < nh; o++) {
@@ -1303,6 +1365,12 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
               }
             }
           }
+          std::vector<int> slot_first(nh + 1, 0);
+          for (size_t t = 0; t < items.size(); t++) slot_first[items[t].slot + 1] = (int)t + 1;
+          for (int o = 0; o < nh; o++) slot_first[o + 1] = std::max(slot_first[o + 1], slot_first[o]);
+          slot_items = call.scratch_n<int>((size_t)nh + 1);
+          STAM_CUDA_CHECK(cudaMemcpyAsync(slot_items, slot_first.data(), sizeof(int) * (nh + 1),
+                                          cudaMemcpyHostToDevice, call.stream()));
           P.nheavy = nh;
           P.heavy_flag = hflag;
           auto* d_hf = call.scratch_n<int64_t>((size_t)(2 * nh));
@@ -1324,7 +1392,7 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
           STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_dense_heavy_kernel,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
           call.before_launch("mttkrp_dense_heavy", aux);
-          mttkrp_dense_heavy_kernel<<<(unsigned)std::min<int64_t>((int64_t)items.size(), (int64_t)sms * 2),
+          mttkrp_dense_heavy_kernel<<<(unsigned)std::min<int64_t>((int64_t)items.size(), (int64_t)sms),
                                       kHvWarps * 32, hsm, aux>>>(P, d_items, (int)items.size(), hclaim,
                                                                 hpart);
           call.after_launch(aux);
@@ -1369,9 +1437,8 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       if (P.nheavy > 0) {
         call.join();
         call.before_launch("mttkrp_dense_heavy_reduce");
-        mttkrp_dense_heavy_reduce_kernel<<<(unsigned)ceil_div((int64_t)P.nheavy * 32, 256), 256, 0,
-                                           call.stream()>>>(P, d_items, (int)items.size(), hpart,
-                                                            heavy_s);
+        mttkrp_dense_heavy_reduce_kernel<<<(unsigned)P.nheavy, 1024, 0, call.stream()>>>(
+            P, slot_items, hpart, heavy_s);
         call.after_launch();
       }
     }
@@ -1399,7 +1466,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     if (Cv->ncols != Dv->ncols) fail(STAM_ERR_DIMENSION_MISMATCH, "mttkrp: C and D ranks differ");
     const int64_t I = B->dims[0], R = Cv->ncols;
     const size_t ws_bytes = (((size_t)R * 8 + (size_t)((R + 31) / 32) * 4) + 15) & ~(size_t)15;
-    const size_t smem = ws_bytes * kSpWarps + sizeof(MatchQueue) * kSpWarps;
+    const size_t smem = ws_bytes * kSpWarps + match_owners_bytes(8) * kSpWarps;
     if (smem > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "sparse mttkrp: rank too large for the shared-memory "
                                        "row workspace in ABI v1 (R <= ~1700)");
@@ -1419,7 +1486,6 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.dpos = call.device_input(Dv->pos, (size_t)Dv->nrows + 1, Dv->mem);
     P.didx = call.device_input(Dv->idx, (size_t)Dv->nnz, Dv->mem);
     P.dvals = call.device_input(Dv->vals, (size_t)Dv->nnz, Dv->mem);
-    const size_t smem_w = ws_bytes * kSpWarps + sizeof(MatchQueue) * kSpWarps;
     P.stage_idx = call.scratch_n<int64_t>((size_t)(I * R));
     P.stage_vals = call.scratch_n<double>((size_t)(I * R));
     auto* ctl = static_cast<uint64_t*>(call.scratch_zero(4 * 8));
@@ -1431,6 +1497,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     // factor-row column bitmaps when R fits W <= 8 words
     const int64_t words = (R + 63) / 64;
     const int W = words <= 1 ? 1 : words <= 2 ? 2 : words <= 4 ? 4 : words <= 8 ? 8 : 0;
+    const size_t smem_w = ws_bytes * kSpWarps + match_owners_bytes(W > 0 ? W : 1) * kSpWarps;
     auto build_bm = [&](const int64_t* pos, const int64_t* idx, int64_t nrows) {
       // rows are read with 256-bit loads (W = 4): align the array to 32 bytes
       auto* raw = call.scratch_n<unsigned long long>((size_t)(nrows * W) + 4);

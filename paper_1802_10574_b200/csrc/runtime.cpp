@@ -171,6 +171,14 @@ int64_t Call::read_scalar(const int64_t* dptr) {
 }
 
 void Call::read_scalars(const int64_t* dptr, int n, int64_t* out) {
+  if (n > ctx_->h_scalars_cap) {
+    STAM_CUDA_CHECK(cudaStreamSynchronize(ctx_->stream));
+    if (ctx_->h_scalars) STAM_CUDA_CHECK(cudaFreeHost(ctx_->h_scalars));
+    ctx_->h_scalars = nullptr;
+    ctx_->h_scalars_cap = 0;
+    STAM_CUDA_CHECK(cudaMallocHost(&ctx_->h_scalars, (size_t)n * sizeof(int64_t)));
+    ctx_->h_scalars_cap = n;
+  }
   STAM_CUDA_CHECK(cudaMemcpyAsync(ctx_->h_scalars, dptr, n * sizeof(int64_t),
                                   cudaMemcpyDeviceToHost, ctx_->stream));
   STAM_CUDA_CHECK(cudaStreamSynchronize(ctx_->stream));
@@ -500,6 +508,7 @@ int stam_cuda_ctx_create(int device, stam_cuda_ctx** out) {
     uint64_t threshold = UINT64_MAX;
     STAM_CUDA_CHECK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     STAM_CUDA_CHECK(cudaMallocHost(&c->h_scalars, 64 * sizeof(int64_t)));
+    c->h_scalars_cap = 64;
     for (int i = 0; i < 64; i++) {
       cudaEvent_t ev;
       STAM_CUDA_CHECK(cudaEventCreate(&ev));

@@ -56,8 +56,9 @@ struct Ctx {
   cudaMemPool_t pool = nullptr;
   // pinned host memory returned by released host results, reused by size
   std::vector<std::pair<void*, size_t>> pinned_free;
-  // small pinned scalars for count read-back
+  // small pinned scalars for count read-back (grown on demand)
   int64_t* h_scalars = nullptr;
+  int h_scalars_cap = 0;
   std::vector<cudaEvent_t> event_pool;
   size_t event_next = 0;
 };

@@ -1205,6 +1205,181 @@ __global__ void gather_keys_kernel(const int64_t* rows, int64_t n, const int64_t
   if (t < n) keys[t] = (uint64_t)prod[rows[t]];
 }
 
+// ---------------------------------------------------------------------------
+// Narrow B (n <= kNarrowCols columns) with short rows (P_i <= pmax): one fused
+// pass, no symbolic kernel, no bins, no scan.  A warp per row of a tile of
+// kNarrowRows consecutive rows: the row's products set bits in a column bitmap
+// of n bits in shared memory (the whole column space: no hashing, the column
+// order is the bit order), a popcount prefix over the words gives every
+// column its slot in the row, the products' values are added at their slots
+// (shared fp64 atomics; first insert into 0.0 as the workspace does), and the
+// tile learns its output offset by decoupled look-back (tiles are claimed in
+// row order) and writes its rows straight into C, which is allocated at the
+// products bound.  Config 1 (10k x 10k, 400 products per row) runs as one
+// kernel plus a products reduction.
+constexpr int kNarrowCols = 16384;
+constexpr int kNarrowRows = 8;  // warps (rows) per CTA tile
+constexpr int kNarrowMaxP = 1024;
+
+__global__ void narrow_products_kernel(const SpgemmParams P, unsigned long long* out) {
+  // out[0] += products, out[1] = max products of a row (a warp per row)
+  const unsigned lane = lane_id();
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long tot = 0, mx = 0;
+  for (int64_t i = warp; i < P.m; i += nwarps) {
+    const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
+    unsigned long long s = 0;
+    for (int64_t p = a0 + lane; p < a1; p += 32) {
+      const int64_t k = P.aidx[p];
+      s += (unsigned long long)(P.bpos[k + 1] - P.bpos[k]);
+    }
+    s = warp_sum(s);
+    tot += s;
+    mx = max(mx, s);
+  }
+  if (lane == 0) {
+    if (tot) atomicAdd(&out[0], tot);
+    atomicMax(&out[1], mx);
+  }
+}
+
+// Enumerates the row's products 32 at a time: f(col, value) per product.
+template <bool kNumeric, typename F>
+__device__ __forceinline__ void narrow_products(const SpgemmParams& P, int64_t a0, int64_t a1,
+                                                F f) {
+  const int lane = (int)lane_id();
+  for (int64_t c = a0; c < a1; c += 32) {
+    const int64_t p = c + lane;
+    int64_t b0 = 0;
+    int len = 0;
+    double av = 0.0;
+    if (p < a1) {
+      const int64_t k = P.aidx[p];
+      b0 = P.bpos[k];
+      len = (int)(P.bpos[k + 1] - b0);
+      if (kNumeric) av = P.avals[p];
+    }
+    const int inc = warp_inclusive_scan(len);
+    const int total = __shfl_sync(kFull, inc, 31);
+    const int off = inc - len;  // first product of lane's entry
+    for (int base = 0; base < total; base += 32 * 4) {
+      int64_t q[4];
+      double a[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int j = base + 32 * u + lane;
+        ok[u] = j < total;
+        // entry holding product j: the last lane whose off <= j
+        int e = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+          const int ov = __shfl_sync(kFull, off, (e + st) & 31);
+          if (ov <= j) e += st;
+        }
+        // (the last lane with off <= j holds products: empty entries share
+        // their offset with the next nonempty one)
+        const int64_t be = __shfl_sync(kFull, b0, e);
+        const int oe = __shfl_sync(kFull, off, e);
+        a[u] = kNumeric ? __shfl_sync(kFull, av, e) : 0.0;
+        q[u] = be + (j - oe);
+      }
+      int64_t col[4];
+      double bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        col[u] = ok[u] ? P.bidx[q[u]] : 0;
+        bv[u] = (kNumeric && ok[u]) ? P.bvals[q[u]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (ok[u]) f(col[u], kNumeric ? mul_rn(a[u], bv[u]) : 0.0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kNarrowRows * 32) spgemm_narrow_kernel(
+    const SpgemmParams P, int nwords, int pmax, uint64_t* status, unsigned long long* claim) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int counts[kNarrowRows];
+  __shared__ int64_t tile_sh, prefix_sh;
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  const size_t per_warp = ((size_t)nwords * 12 + (size_t)pmax * 8 + 15) & ~(size_t)15;
+  unsigned char* mine = smem_raw + per_warp * warp;
+  double* vals = reinterpret_cast<double*>(mine);
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(mine + (size_t)pmax * 8);
+  int* wpre = reinterpret_cast<int*>(bits + nwords);
+  for (int w = lane; w < nwords; w += 32) bits[w] = 0ull;
+  const int64_t ntiles = (P.m + kNarrowRows - 1) / kNarrowRows;
+  while (true) {
+    if (threadIdx.x == 0) tile_sh = (int64_t)atomicAdd(claim, 1ull);
+    __syncthreads();
+    const int64_t tile = tile_sh;
+    if (tile >= ntiles) break;
+    const int64_t i = tile * kNarrowRows + warp;
+    int count = 0;
+    if (i < P.m) {
+      const int64_t a0 = P.apos[i], a1 = P.apos[i + 1];
+      narrow_products<false>(P, a0, a1, [&](int64_t col, double) {
+        atomicOr(&bits[col >> 6], 1ull << (col & 63));
+      });
+      __syncwarp();
+      int run = 0;
+      for (int w0 = 0; w0 < nwords; w0 += 32) {
+        const int w = w0 + lane;
+        const int c = w < nwords ? __popcll(bits[w]) : 0;
+        const int inc = warp_inclusive_scan(c);
+        if (w < nwords) wpre[w] = run + inc - c;
+        run += __shfl_sync(kFull, inc, 31);
+      }
+      count = run;
+      if (P.values) {
+        for (int t = lane; t < count; t += 32) vals[t] = 0.0;
+        __syncwarp();
+        narrow_products<true>(P, a0, a1, [&](int64_t col, double v) {
+          const int w = (int)(col >> 6);
+          const int slot = wpre[w] + __popcll(bits[w] & ((1ull << (col & 63)) - 1ull));
+          atomicAdd(&vals[slot], v);
+        });
+      }
+    }
+    if (lane == 0) counts[warp] = count;
+    __syncthreads();
+    if (warp == 0) {
+      const int c = lane < kNarrowRows ? counts[lane] : 0;
+      const int64_t agg = warp_sum((int64_t)c);
+      const int64_t ex = lookback_exclusive(status, tile, agg);
+      if (lane == 0) prefix_sh = ex;
+    }
+    __syncthreads();
+    if (i < P.m) {
+      int64_t off = prefix_sh;
+      for (int w = 0; w < warp; w++) off += counts[w];
+      if (lane == 0) {
+        P.cpos[i] = off;
+        if (i == P.m - 1) P.cpos[P.m] = off + count;
+      }
+      // columns: a lane per bitmap word (its bits in order), values coalesced
+      for (int w = lane; w < nwords; w += 32) {
+        unsigned long long b = bits[w];
+        int pos = wpre[w];
+        while (b) {
+          const int bit = __ffsll((long long)b) - 1;
+          P.cidx[off + pos] = (int64_t)w * 64 + bit;
+          pos++;
+          b &= b - 1;
+        }
+        bits[w] = 0ull;  // ready for the next row
+      }
+      if (P.values)
+        for (int t = lane; t < count; t += 32) P.cvals[off + t] = vals[t];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 }  // namespace stamgpu
 
@@ -1283,6 +1458,73 @@ void bin_rows(stamrt::Call& call, SpgemmParams& P, const int64_t* host,
 }  // namespace
 }  // namespace stamgpu
 
+namespace stamgpu {
+namespace {
+// Narrow path (spgemm_narrow_kernel): returns false (nothing launched that
+// matters) when a row has more than kNarrowMaxP products.
+bool spgemm_narrow(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
+                   stam_csr_result* Cr) {
+  using stamrt::ceil_div;
+  const int64_t m = A->nrows, n = B->ncols;
+  SpgemmParams P{};
+  P.m = m;
+  P.n = n;
+  P.apos = call.device_input(A->pos, (size_t)m + 1, A->mem);
+  P.aidx = call.device_input(A->idx, (size_t)A->nnz, A->mem);
+  P.avals = call.device_input(A->vals, (size_t)A->nnz, A->mem);
+  P.bpos = call.device_input(B->pos, (size_t)B->nrows + 1, B->mem);
+  P.bidx = call.device_input(B->idx, (size_t)B->nnz, B->mem);
+  P.bvals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
+  const int sms = call.ctx()->num_sms;
+  const int64_t ntiles = ceil_div(m, (int64_t)kNarrowRows);
+  // control block: [0] products, [1] max products, [2] tile claims, then tile status
+  auto* ctl = static_cast<unsigned long long*>(
+      call.scratch_zero(sizeof(unsigned long long) * (size_t)(4 + ntiles)));
+  call.before_launch("spgemm_narrow_products");
+  narrow_products_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)sms * 8), 256, 0,
+                           call.stream()>>>(P, ctl);
+  call.after_launch();
+  int64_t hv[2];
+  call.read_scalars(reinterpret_cast<const int64_t*>(ctl), 2, hv);
+  const int64_t products = hv[0], pmax_row = hv[1];
+  if (pmax_row > kNarrowMaxP) return false;
+  const int nwords = (int)ceil_div(n, (int64_t)64);
+  const int pmax = (int)std::max<int64_t>(32, (pmax_row + 31) / 32 * 32);
+  const size_t smem = (((size_t)nwords * 12 + (size_t)pmax * 8 + 15) & ~(size_t)15) * kNarrowRows;
+  if (smem > call.ctx()->smem_optin) return false;
+  P.values = call.opts().mode == STAM_MODE_FUSED;
+  P.sorted = true;
+  call.alloc_csr_result(Cr, m, n, products);
+  P.cpos = Cr->pos;
+  P.cidx = Cr->idx;
+  P.cvals = Cr->vals;
+  if (!P.values && products > 0)  // ASSEMBLE: index only, values defined as zero
+    STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)products, call.stream()));
+  if (m == 0) STAM_CUDA_CHECK(cudaMemsetAsync(Cr->pos, 0, sizeof(int64_t), call.stream()));
+  STAM_CUDA_CHECK(cudaFuncSetAttribute(spgemm_narrow_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spgemm_narrow_kernel,
+                                                                kNarrowRows * 32, smem));
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, per_sm) * sms);
+  call.before_launch("spgemm_narrow");
+  spgemm_narrow_kernel<<<(unsigned)grid, kNarrowRows * 32, smem, call.stream()>>>(
+      P, nwords, pmax, reinterpret_cast<uint64_t*>(ctl + 4), ctl + 2);
+  call.after_launch();
+  const int64_t nnz = call.read_scalar(Cr->pos + m);
+  call.finish_csr_result(Cr, nnz);
+  call.finish();
+  stam_stats* st = call.stats();
+  st->mults = products;
+  st->adds = products;
+  st->ws_inserts = products;
+  st->ws_resets = m;
+  st->appends = nnz;
+  return true;
+}
+}  // namespace
+}  // namespace stamgpu
+
 extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, const stam_csr_view* B,
                                 const stam_options* opts, stam_csr_result* Cr, stam_stats* stats) {
   using namespace stamgpu;
@@ -1298,6 +1540,8 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
       fail(STAM_ERR_UNSUPPORTED_MERGE, "spgemm: B has 2^32 or more columns");
     const int64_t m = A->nrows, n = B->ncols;
     SpgemmParams P;
+    if (n <= kNarrowCols && spgemm_narrow(call, A, B, Cr))
+      return;
     int64_t host[16];
     prepare(call, A, B, P, host);
     P.values = call.opts().mode == STAM_MODE_FUSED;

@@ -28,7 +28,9 @@ def main():
     W.cid = args.config
     W.name = G.CONFIG_NAMES[args.config]
     W.cfg = G.make_config(args.config, scale=args.scale)
+    W.broadcast_ms, W.broadcast_bytes = 0.0, 0
     ctx = Context(0)
+    W.distribute(1, 0, False)
     W.setup(ctx)
     for _ in range(args.steps):
         W.step()
