@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -43,11 +44,6 @@
 namespace stamgpu {
 namespace {
 
-// Runtime switch for A/B measurements of alternative paths (default on).
-inline bool env_flag(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) != 0 : dflt != 0;
-}
 
 // ===========================================================================
 // dense
@@ -70,17 +66,8 @@ struct DenseParams {
   unsigned long long* counter;  // dynamic chunk claims
   double* part;         // [ncb][nchunks][2][32] partials (head, tail)
   int64_t* part_slice;  // [nchunks][2]: head slice (-1 none, -2 empty chunk), tail slice
-  // heavy slices (computed by mttkrp_dense_heavy_kernel; skipped by the chunked kernels)
-  int nheavy;
-  const int64_t* heavy_f;     // [nheavy][2] fiber range of each heavy slice
-  const unsigned char* heavy_flag;  // [I] 1 for a heavy slice
 };
 
-__device__ __forceinline__ bool fiber_is_heavy(const DenseParams& P, int64_t f) {
-  bool h = false;
-  for (int t = 0; t < P.nheavy; t++) h |= (f >= P.heavy_f[2 * t]) && (f < P.heavy_f[2 * t + 1]);
-  return h;
-}
 
 __device__ __forceinline__ int64_t lower_bound_g(const int64_t* a, int64_t n, int64_t x) {
   int64_t lo = 0;
@@ -191,7 +178,6 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
         t[x] += __shfl_xor_sync(kFull, t[x], 16);
         acc[x] = 0.0;
       }
-      if (P.nheavy && P.heavy_flag[st.s]) return;  // mttkrp_dense_heavy_kernel's row
       const bool started_here = !st.open;
       double* dst;
       if (started_here && ends_here) {
@@ -215,7 +201,6 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
         mj = (int)P.idx1[fg + lane];
         mz = P.pos2[fg + lane];
         mlen = (int)(P.pos2[fg + lane + 1] - mz);
-        if (P.nheavy && fiber_is_heavy(P, fg + lane)) mlen = 0;  // tiled kernel's fiber
       }
       // Steps: up to 4 consecutive short fibers, a quarter each; or one long
       // fiber (>= kLongFiber nonzeros) split over all four quarters (batch t
@@ -285,6 +270,23 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
               bn = P.vals[z0 + zl];
             }
           }
+          if (!lmode && nmax - zb == 1) {
+            // every quarter holds at most one nonzero (the typical short-fiber
+            // step): one row load per lane, no unused slots
+            const int k = __shfl_sync(kFull, kk, qbase);
+            const double bv = __shfl_sync(kFull, bb, qbase);
+            if (zb < len) {
+              double2 d0, d1;
+              ld_row32<k256>(P.D + (int64_t)k * 32 + col, d0, d1);
+              w[0] = fma(bv, d0.x, w[0]);
+              w[1] = fma(bv, d0.y, w[1]);
+              w[2] = fma(bv, d1.x, w[2]);
+              w[3] = fma(bv, d1.y, w[3]);
+            }
+            kk = kn;
+            bb = bn;
+            continue;
+          }
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             if (__all_sync(kFull, zb + zoff + 4 * h >= len)) break;  // no quarter has entries left
@@ -348,288 +350,8 @@ __global__ void __launch_bounds__(256, DQ_MINB) mttkrp_dense32q_kernel(const Den
     if (fb < st.s_end) flush(false);
     if (lane == 0) {
       if (!st.wrote_head) P.part_slice[2 * c] = -1;
-      if (!(fb < st.s_end && !st.open) || (P.nheavy && P.heavy_flag[st.s]))
-        P.part_slice[2 * c + 1] = -1;
+      if (!(fb < st.s_end && !st.open)) P.part_slice[2 * c + 1] = -1;
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Heavy slices (R == 32): slices whose fibers are long enough that D rows
-// repeat many times inside a block of fibers (config 4's top slices: fibers of
-// ~3,200 / 1,100 / 600 nonzeros over K = 28,818).  Work items are blocks of
-// kHvFibers consecutive fibers of one heavy slice times a range of k.  A CTA
-// walks its item's k range in tiles of kHvTile D rows; each tile is copied
-// global -> shared by one cp.async.bulk (TMA, 48 KB contiguous: D is
-// row-major) on an mbarrier, double-buffered so the next tile lands while this
-// one is consumed.  Every quarter-warp owns 4 fibers and consumes, per tile,
-// the nonzeros whose k falls inside it, reading D from shared memory: each D
-// row is fetched from L2 once per item instead of once per nonzero (the
-// chunked kernel's 256 B per nonzero).  A fiber's w0 partial over the item's k
-// range is multiplied into C(j,:) and summed (fixed order) into the item's
-// partial row; mttkrp_dense_heavy_reduce adds an item's partials per slice in
-// item order (deterministic).
-#ifndef HV_FPQ
-#define HV_FPQ 2
-#endif
-constexpr int kHvWarps = 16;
-constexpr int kHvFpq = HV_FPQ;                      // fibers per quarter-warp
-constexpr int kHvFibers = kHvWarps * 4 * kHvFpq;   // fibers per work item
-constexpr int kHvDepth = 3;                          // batches of 8 nonzeros held per fiber
-#ifndef HV_TILE
-#define HV_TILE 192
-#endif
-constexpr int kHvTile = HV_TILE;  // D rows per stage (48 KB at R = 32)
-
-struct HeavyItem {
-  int64_t f0, f1;  // fibers [f0, f1), f1 - f0 <= kHvFibers, one slice
-  int32_t k0, k1;  // k range [k0, k1)
-  int32_t slot;    // heavy slice index
-  int32_t pad;
-};
-
-struct HeavySmem {
-  double tile[2][kHvTile * 32];
-  double red[kHvWarps][32];
-  uint64_t bar[2];
-  int item;
-};
-
-// Quarter-cooperative lower bound: first z in [z0, z1) with idx2[z] >= k.
-// Every quarter of the warp searches its own range; the loop runs while any
-// quarter is still narrowing (ballots are warp-wide).
-__device__ __forceinline__ int64_t quarter_lower_bound(const int64_t* idx2, int64_t z0, int64_t z1,
-                                                       int64_t k, int ql, unsigned qmask) {
-  int64_t lo = z0, hi = z1;  // answer in [lo, hi]
-  while (__any_sync(kFull, hi - lo > 8)) {
-    const bool act = hi - lo > 8;  // uniform within the quarter
-    const int64_t step = act ? (hi - lo + 7) >> 3 : 0;
-    const int64_t p = lo + (int64_t)ql * step;
-    const bool lt = act && p < hi && idx2[p] < k;
-    const int nlt = __popc(__ballot_sync(kFull, lt) & qmask);  // samples below k: a prefix
-    if (act) {
-      if (nlt == 0) {
-        hi = lo;
-      } else {
-        lo = lo + (int64_t)(nlt - 1) * step + 1;
-        hi = min(hi, lo - 1 + step);
-      }
-    }
-  }
-  // final pass over <= 8 candidates
-  const int64_t p = lo + ql;
-  const bool lt = p < hi && idx2[p] < k;
-  return lo + __popc(__ballot_sync(kFull, lt) & qmask);
-}
-
-__global__ void __launch_bounds__(kHvWarps * 32, 1) mttkrp_dense_heavy_kernel(
-    const DenseParams P, const HeavyItem* items, int nitems, unsigned long long* claim,
-    double* hpart) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  HeavySmem& S = *reinterpret_cast<HeavySmem*>(smem_raw);
-  const int lane = (int)lane_id();
-  const int warp = threadIdx.x >> 5;
-  const int q = lane >> 3, ql = lane & 7;
-  const int qbase = lane & ~7;
-  const unsigned qmask = 0xffu << qbase;
-  // lane columns: 2ql, 2ql+1 and 16+2ql, 16+2ql+1 (a quarter's 16-byte loads
-  // of one row are contiguous: conflict-free shared reads)
-  const int ca = 2 * ql, cb = 16 + 2 * ql;
-  if (threadIdx.x == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t gt = 0;  // tiles consumed by this CTA (stage = gt & 1, parity = (gt >> 1) & 1)
-  auto issue = [&](const HeavyItem& it, int t, uint32_t g) {
-    const int kt0 = it.k0 + t * kHvTile;
-    const int rows = min(kHvTile, it.k1 - kt0);
-    const uint32_t bytes = (uint32_t)rows * 256u;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&S.bar[g & 1], bytes);
-    bulk_g2s(S.tile[g & 1], P.D + (int64_t)kt0 * 32, bytes, &S.bar[g & 1]);
-  };
-  while (true) {
-    if (threadIdx.x == 0) S.item = (int)atomicAdd(claim, 1ull);
-    __syncthreads();
-    const int itn = S.item;
-    if (itn >= nitems) break;
-    const HeavyItem it = items[itn];
-    const int nt = (it.k1 - it.k0 + kHvTile - 1) / kHvTile;
-    if (threadIdx.x == 0) {
-      issue(it, 0, gt);
-      if (nt > 1) issue(it, 1, gt + 1);
-    }
-    // this quarter's fibers: kHvDepth batches of 8 nonzeros in flight (lane ql
-    // holds entry cur + 8d + ql of batch d); batch 0 is being consumed
-    int64_t cur[kHvFpq];
-    int32_t zrem[kHvFpq];  // entries from cur to the fiber's end
-    int used[kHvFpq];
-    int kb[kHvFpq][kHvDepth];
-    double bb[kHvFpq][kHvDepth];
-    double w[kHvFpq][4];
-#pragma unroll
-    for (int u = 0; u < kHvFpq; u++) {
-      const int64_t f = it.f0 + (warp * 4 + q) * kHvFpq + u;
-      int64_t z0 = 0, z1 = 0;
-      if (f < it.f1) {
-        z0 = P.pos2[f];
-        z1 = P.pos2[f + 1];
-      }
-      if (it.k0 > 0) z0 = quarter_lower_bound(P.idx2, z0, z1, it.k0, ql, qmask);
-      cur[u] = z0;
-      zrem[u] = (int32_t)(z1 - z0);
-      used[u] = 0;
-#pragma unroll
-      for (int d = 0; d < kHvDepth; d++) {
-        const int e = 8 * d + ql;
-        kb[u][d] = e < zrem[u] ? (int)P.idx2[z0 + e] : INT_MAX;
-        bb[u][d] = e < zrem[u] ? P.vals[z0 + e] : 0.0;
-      }
-#pragma unroll
-      for (int x = 0; x < 4; x++) w[u][x] = 0.0;
-    }
-    for (int t = 0; t < nt; t++, gt++) {
-      const int kt0 = it.k0 + t * kHvTile;
-      const int kt1 = min(it.k1, kt0 + kHvTile);
-      mbar_wait_parity(&S.bar[gt & 1], (gt >> 1) & 1);
-      const double* tile = S.tile[gt & 1];
-#pragma unroll
-      for (int u = 0; u < kHvFpq; u++) {
-        while (true) {
-          // entries [used, 8) of batch 0 with k < kt1 (a prefix: k sorted)
-          const bool in = ql >= used[u] && kb[u][0] < kt1;
-          const unsigned m = (__ballot_sync(kFull, in) & qmask) >> qbase;
-          const int n = __popc(m);
-          const int nmax = __reduce_max_sync(kFull, (unsigned)n);
-          if (nmax == 0) break;  // uniform
-          for (int e0 = 0; e0 < nmax; e0 += 4) {
-            double2 da[4], db[4];
-            double b[4];
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-              const int e = e0 + v;
-              const int src = qbase + min(7, used[u] + e);
-              const int k = __shfl_sync(kFull, kb[u][0], src);
-              const double bv = __shfl_sync(kFull, bb[u][0], src);
-              const bool ok = e < n;
-              b[v] = ok ? bv : 0.0;
-              const double* row = tile + (ok ? (k - kt0) : 0) * 32;
-              da[v] = *reinterpret_cast<const double2*>(row + ca);
-              db[v] = *reinterpret_cast<const double2*>(row + cb);
-            }
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-              w[u][0] = fma(b[v], da[v].x, w[u][0]);
-              w[u][1] = fma(b[v], da[v].y, w[u][1]);
-              w[u][2] = fma(b[v], db[v].x, w[u][2]);
-              w[u][3] = fma(b[v], db[v].y, w[u][3]);
-            }
-          }
-          used[u] += n;
-          // a fully consumed batch: shift the ring, prefetch kHvDepth batches ahead
-          const bool adv = used[u] == 8;
-          if (adv) {
-            cur[u] += 8;
-            zrem[u] -= 8;
-            used[u] = 0;
-#pragma unroll
-            for (int d = 0; d + 1 < kHvDepth; d++) {
-              kb[u][d] = kb[u][d + 1];
-              bb[u][d] = bb[u][d + 1];
-            }
-            const int e = 8 * (kHvDepth - 1) + ql;
-            kb[u][kHvDepth - 1] = e < zrem[u] ? (int)P.idx2[cur[u] + e] : INT_MAX;
-            bb[u][kHvDepth - 1] = e < zrem[u] ? P.vals[cur[u] + e] : 0.0;
-          }
-          if (!__any_sync(kFull, adv)) break;
-        }
-      }
-      __syncthreads();  // every warp is done with this stage
-      if (threadIdx.x == 0 && t + 2 < nt) issue(it, t + 2, gt + 2);
-    }
-    // w0 (partial over [k0, k1)) x C(j,:), summed over the quarter's fibers,
-    // the warp's quarters and the CTA's warps in a fixed order
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int u = 0; u < kHvFpq; u++) {
-      const int64_t f = it.f0 + (warp * 4 + q) * kHvFpq + u;
-      if (f < it.f1) {
-        const int64_t j = P.idx1[f];
-        const double2 c0 = __ldg(reinterpret_cast<const double2*>(P.C + j * 32 + ca));
-        const double2 c1 = __ldg(reinterpret_cast<const double2*>(P.C + j * 32 + cb));
-        acc[0] = fma(w[u][0], c0.x, acc[0]);
-        acc[1] = fma(w[u][1], c0.y, acc[1]);
-        acc[2] = fma(w[u][2], c1.x, acc[2]);
-        acc[3] = fma(w[u][3], c1.y, acc[3]);
-      }
-    }
-#pragma unroll
-    for (int x = 0; x < 4; x++) {
-      acc[x] += __shfl_xor_sync(kFull, acc[x], 8);
-      acc[x] += __shfl_xor_sync(kFull, acc[x], 16);
-    }
-    if (q == 0) {
-      S.red[warp][ca] = acc[0];
-      S.red[warp][ca + 1] = acc[1];
-      S.red[warp][cb] = acc[2];
-      S.red[warp][cb + 1] = acc[3];
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double sum = 0.0;
-#pragma unroll
-      for (int x = 0; x < kHvWarps; x++) sum += S.red[x][lane];
-      hpart[(int64_t)itn * 32 + lane] = sum;
-    }
-  }
-}
-
-// Heavy slice rows: a CTA per slice; warp w adds the slice's items w, w+32,
-// ... in order, then warp 0 adds the 32 warp sums in order (deterministic).
-__global__ void mttkrp_dense_heavy_reduce_kernel(const DenseParams P, const int* slot_items,
-                                                 const double* hpart, const int64_t* heavy_s) {
-  __shared__ double ws[32][33];
-  const int lane = (int)lane_id();
-  const int warp = threadIdx.x >> 5;
-  const int hs = blockIdx.x;
-  const int t0 = slot_items[hs], t1 = slot_items[hs + 1];
-  double sum = 0.0;
-  for (int t = t0 + warp; t < t1; t += 32) sum += hpart[(int64_t)t * 32 + lane];
-  ws[warp][lane] = sum;
-  __syncthreads();
-  if (warp == 0) {
-    double tot = 0.0;
-    for (int x = 0; x < 32; x++) tot += ws[x][lane];
-    P.A[heavy_s[hs] * 32 + lane] = tot;
-  }
-}
-
-// Per-slice nnz and fibers; slices whose average fiber is long enough for a
-// block of kHvFibers fibers to reuse each staged D row (avg length > 2K /
-// kHvFibers) and that hold at least one full block are listed as heavy.
-constexpr int kMaxHeavy = 64;
-__global__ void mttkrp_dense_heavy_select_kernel(const DenseParams P, int64_t min_len,
-                                                 unsigned char* flag, int64_t* list,
-                                                 unsigned long long* count) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.I;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
-    const int64_t nz = f1 > f0 ? P.pos2[f1] - P.pos2[f0] : 0;
-    bool heavy = f1 - f0 >= kHvFibers && nz >= min_len * (f1 - f0);
-    if (heavy) {
-      const unsigned long long at = atomicAdd(count, 1ull);
-      if (at < kMaxHeavy) {
-        list[4 * at] = i;
-        list[4 * at + 1] = f0;
-        list[4 * at + 2] = f1;
-        list[4 * at + 3] = nz;
-      } else {
-        heavy = false;
-      }
-    }
-    flag[i] = heavy ? 1 : 0;
   }
 }
 
@@ -1001,6 +723,19 @@ __device__ __forceinline__ void load_bm(const unsigned long long* p, unsigned lo
   }
 }
 
+// Factor value / row-pointer gathers at matches.  Only the bitmaps (32 MB at
+// config 5) are kept evict_last: the whole gathered set (bitmaps + values +
+// row pointers, ~104 MB) does not stay resident beside the 6.4 GB stream.
+#ifndef SP_VAL_HINT
+#define SP_VAL_HINT 0  // 0 normal, 1 evict_last, 2 evict_first
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_val(const T* p, uint64_t keep) {
+  if constexpr (SP_VAL_HINT == 1) return ld_keep(p, keep);
+  else if constexpr (SP_VAL_HINT == 2) return __ldcs(p);
+  else return __ldg(p);
+}
+
 // load_bm with the L2 evict_last hint (the bitmaps are re-read ~400 times per
 // call while the CSF streams past them once).
 template <int W>
@@ -1029,34 +764,40 @@ __device__ __forceinline__ int bm_rank(const unsigned long long (&b)[W], int r) 
   return n;
 }
 
-// Matches (C_j ∩ D_k columns of single-nonzero fibers) are expanded warp-
-// cooperatively: every lane with matches parks its fiber's (C row start, D
-// row start, b, match / C / D bitmaps) in a per-warp shared buffer, then the
-// warp's matches are numbered (a warp scan) and taken 32 at a time, lane s
-// evaluating match s: owner lane by a shuffle search over the scan, the
-// owner's t-th matched column by popcounts over its bitmap, the value
-// positions by popcounts of the C and D bitmaps below it.  No per-lane bit
-// walk (a lane with two matches no longer holds 31 others back).
-template <int W>
-struct MatchOwners {
-  int64_t c0[32];
-  int64_t d0[32];
-  double b[32];
-  unsigned long long m[W][32];
-  unsigned long long bc[W][32];
-  unsigned long long bd[W][32];
+// Matches (C_j ∩ D_k columns of single-nonzero fibers) are queued per warp
+// so that their value gathers and workspace updates run on full warps instead
+// of the few lanes that found a match.  (A warp-cooperative expansion -- lane
+// s evaluating the warp's s-th match, owner found by a shuffle search -- cut
+// no time: 6.79 vs 6.22 ms at config 5, the kernel waits on memory.)
+constexpr int kQ = 128;
+struct MatchQueue {
+  int64_t ci[kQ];  // position of C(j,r) in C's values
+  int64_t di[kQ];  // position of D(k,r) in D's values
+  double b[kQ];    // B(i,j,k)
+  int r[kQ];
 };
-__host__ __device__ constexpr size_t match_owners_bytes(int W) { return (size_t)(3 + 3 * W) * 32 * 8; }
+
+__host__ __device__ constexpr size_t match_queue_bytes() { return sizeof(MatchQueue); }
 
 // sparse_slice with factor-row bitmaps: C_j ∩ D_k is a word-wise AND and a
 // matched column's value positions are popcounts (same arithmetic and
 // per-entry order as sparse_slice: w0 = 0 + b*D(k,r), w1(r) += w0*C(j,r)).
 template <int W>
 __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, uint32_t* wb,
-                                unsigned long long& mults, MatchOwners<W>& O) {
+                                unsigned long long& mults, void* mbuf) {
   const int lane = (int)lane_id();
   const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
   const uint64_t keep = l2_evict_last_policy();
+  MatchQueue& Q = *static_cast<MatchQueue*>(mbuf);
+  int qn = 0;  // queued matches (warp-uniform)
+  auto flush = [&]() {
+    for (int t = lane; t < qn; t += 32) {
+      const double w0 = add_rn(0.0, mul_rn(Q.b[t], ld_val(P.dvals + Q.di[t], keep)));
+      ws_add(wv, wb, Q.r[t], mul_rn(w0, ld_val(P.cvals + Q.ci[t], keep)));
+    }
+    __syncwarp();
+    qn = 0;
+  };
   for (int64_t fb = f0; fb < f1; fb += 32) {
     const int64_t f = fb + lane;
     int nm = 0;
@@ -1122,61 +863,46 @@ __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, ui
     const int inc = warp_inclusive_scan(nm);
     const int tot = __shfl_sync(kFull, inc, 31);
     if (tot == 0) continue;
+    // per-lane walk of the matched bits into the warp's queue (evaluated 32 at
+    // a time by flush), or directly when the batch alone overflows the queue
+    if (tot > kQ - qn) flush();
+    const bool direct = tot > kQ;
     if (nm > 0) {
-      O.c0[lane] = ld_keep(P.cpos + j, keep);
-      O.d0[lane] = ld_keep(P.dpos + k, keep);
-      O.b[lane] = b;
+      const int64_t c0 = ld_val(P.cpos + j, keep), d0 = ld_val(P.dpos + k, keep);
+      int slot = qn + inc - nm;
+      int rc = 0, rd = 0;
 #pragma unroll
       for (int w = 0; w < W; w++) {
-        O.m[w][lane] = m[w];
-        O.bc[w][lane] = bc[w];
-        O.bd[w][lane] = bd[w];
+        unsigned long long mm = m[w];
+        while (mm) {
+          const int bit = __ffsll((long long)mm) - 1;
+          const unsigned long long below = (1ull << bit) - 1ull;
+          const int64_t ci = c0 + rc + __popcll(bc[w] & below);
+          const int64_t di = d0 + rd + __popcll(bd[w] & below);
+          if (direct) {
+            const double w0 = add_rn(0.0, mul_rn(b, ld_val(P.dvals + di, keep)));
+            ws_add(wv, wb, w * 64 + bit, mul_rn(w0, ld_val(P.cvals + ci, keep)));
+          } else {
+            Q.ci[slot] = ci;
+            Q.di[slot] = di;
+            Q.b[slot] = b;
+            Q.r[slot] = w * 64 + bit;
+            slot++;
+          }
+          mults++;
+          mm &= mm - 1ull;
+        }
+        rc += __popcll(bc[w]);
+        rd += __popcll(bd[w]);
       }
     }
     __syncwarp();
-    mults += (unsigned long long)nm;
-    for (int g0 = 0; g0 < tot; g0 += 32) {  // warp-uniform
-      const int g = g0 + lane;
-      // owner: the lowest lane whose inclusive count exceeds g
-      int o = 0;
-#pragma unroll
-      for (int st = 16; st >= 1; st >>= 1) {
-        const int iv = __shfl_sync(kFull, inc, (o + st - 1) & 31);
-        if (iv <= g) o += st;
-      }
-      const int ex = __shfl_sync(kFull, inc, o) - __shfl_sync(kFull, nm, o);
-      if (g < tot) {
-        int t = g - ex;  // the owner's t-th match
-        int r = 0, below_c = 0, below_d = 0;
-        bool found = false;
-#pragma unroll
-        for (int w = 0; w < W; w++) {
-          const unsigned long long mw = O.m[w][o];
-          const unsigned long long cw = O.bc[w][o], dw = O.bd[w][o];
-          const int pc = __popcll(mw);
-          if (!found && t < pc) {
-            // t-th set bit of mw (32-bit halves: __fns)
-            const unsigned lo = (unsigned)mw;
-            const int plo = __popc(lo);
-            const int bit = t < plo ? (int)__fns(lo, 0, t + 1)
-                                    : 32 + (int)__fns((unsigned)(mw >> 32), 0, t - plo + 1);
-            const unsigned long long bl = (1ull << bit) - 1ull;
-            r = w * 64 + bit;
-            below_c += __popcll(cw & bl);
-            below_d += __popcll(dw & bl);
-            found = true;
-          } else if (!found) {
-            t -= pc;
-            below_c += __popcll(cw);
-            below_d += __popcll(dw);
-          }
-        }
-        const double w0 = add_rn(0.0, mul_rn(O.b[o], ld_keep(P.dvals + O.d0[o] + below_d, keep)));
-        ws_add(wv, wb, r, mul_rn(w0, ld_keep(P.cvals + O.c0[o] + below_c, keep)));
-      }
+    if (!direct) {
+      qn += tot;
+      if (qn >= kQ - 32) flush();
     }
-    __syncwarp();  // the owner buffer is rewritten by the next batch
   }
+  flush();
 }
 
 // Each warp claims slices dynamically, evaluates one into its shared-memory
@@ -1189,7 +915,7 @@ __device__ void sparse_slice_bm(const SparseParams& P, int64_t i, double* wv, ui
 #endif
 template <int W>
 __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(const SparseParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
   const int64_t R = P.R;
@@ -1197,8 +923,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
   const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
   double* wv = reinterpret_cast<double*>(smem_raw + (size_t)warp * ws_bytes);
   uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
-  auto* owners = reinterpret_cast<MatchOwners<(W > 0 ? W : 1)>*>(
-      smem_raw + (size_t)kSpWarps * ws_bytes + (size_t)warp * match_owners_bytes(W > 0 ? W : 1));
+  void* owners = smem_raw + (size_t)kSpWarps * ws_bytes + (size_t)warp * match_queue_bytes();
   unsigned long long mults = 0;
   while (true) {
     int64_t i = 0;
@@ -1209,7 +934,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
     for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
     __syncwarp();
     if constexpr (W > 0)
-      sparse_slice_bm<W>(P, i, wv, wb, mults, *owners);
+      sparse_slice_bm<W>(P, i, wv, wb, mults, owners);
     else
       sparse_slice(P, i, wv, wb, mults);
     __syncwarp();
@@ -1312,93 +1037,6 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       call.before_launch("mttkrp_dense_bounds");
       mttkrp_dense_bounds_kernel<<<(unsigned)ceil_div(P.nchunks + 1, 256), 256, 0, call.stream()>>>(P);
       call.after_launch();
-      // heavy slices -> the TMA-tiled kernel (beside the chunked one)
-      const bool a16 = ((uintptr_t)P.D % 16 == 0);
-      std::vector<HeavyItem> items;
-      int64_t* heavy_s = nullptr;
-      double* hpart = nullptr;
-      HeavyItem* d_items = nullptr;
-      int* slot_items = nullptr;
-#ifndef HV_DISABLE
-      if (fast && a16 && P.K >= 4 * kHvTile && env_flag("STAM_HV", 1)) {
-        auto* hflag = static_cast<unsigned char*>(call.scratch((size_t)I));
-        auto* hlist = static_cast<int64_t*>(call.scratch_zero(sizeof(int64_t) * (4 * kMaxHeavy + 1)));
-        auto* hcount = reinterpret_cast<unsigned long long*>(hlist + 4 * kMaxHeavy);
-        const int64_t min_len = std::max<int64_t>(64, ceil_div(2 * P.K, (int64_t)kHvFibers));
-        call.before_launch("mttkrp_dense_heavy_select");
-        mttkrp_dense_heavy_select_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 256), (int64_t)sms * 8),
-                                           256, 0, call.stream()>>>(P, min_len, hflag, hlist, hcount);
-        call.after_launch();
-        int64_t hl[4 * kMaxHeavy + 1];
-        call.read_scalars(hlist, 4 * kMaxHeavy + 1, hl);
-        const int nh = (int)std::min<int64_t>(hl[4 * kMaxHeavy], kMaxHeavy);
-        if (nh > 0) {
-          // heaviest first; fiber blocks of kHvFibers, each split over k so an
-          // item holds ~1/4 of a fair share of the heavy nonzeros per CTA slot
-          std::vector<int> order(nh);
-          for (int h = 0; h < nh; h++) order[h] = h;
-          std::sort(order.begin(), order.end(), [&](int a, int b) { return hl[4 * a + 3] > hl[4 * b + 3]; });
-          int64_t hnz = 0;
-          for (int h = 0; h < nh; h++) hnz += hl[4 * h + 3];
-          const int64_t target = std::max<int64_t>(16384, hnz / ((int64_t)sms * 4));
-          std::vector<int64_t> hs(nh), hf(2 * nh);
-          const int64_t ktiles = ceil_div(P.K, (int64_t)kHvTile);
-          for (int o = 0; o < nh; o++) {
-            const int h = order[o];
-            hs[o] = hl[4 * h];
-            hf[2 * o] = hl[4 * h + 1];
-            hf[2 * o + 1] = hl[4 * h + 2];
-            const int64_t nf = hf[2 * o + 1] - hf[2 * o];
-            const double per_fiber = (double)hl[4 * h + 3] / (double)nf;
-            for (int64_t b0 = hf[2 * o]; b0 < hf[2 * o + 1]; b0 += kHvFibers) {
-              const int64_t b1 = std::min<int64_t>(hf[2 * o + 1], b0 + kHvFibers);
-              const int64_t est = (int64_t)(per_fiber * (double)(b1 - b0));
-              const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(ktiles, (est + target / 2) / target));
-              for (int64_t p = 0; p < ks; p++) {
-                HeavyItem itm{};
-                itm.f0 = b0;
-                itm.f1 = b1;
-                itm.k0 = (int32_t)std::min<int64_t>(P.K, ktiles * p / ks * kHvTile);
-                itm.k1 = (int32_t)std::min<int64_t>(P.K, ktiles * (p + 1) / ks * kHvTile);
-                itm.slot = o;
-                if (itm.k1 > itm.k0) items.push_back(itm);
-              }
-            }
-          }
-          std::vector<int> slot_first(nh + 1, 0);
-          for (size_t t = 0; t < items.size(); t++) slot_first[items[t].slot + 1] = (int)t + 1;
-          for (int o = 0; o < nh; o++) slot_first[o + 1] = std::max(slot_first[o + 1], slot_first[o]);
-          slot_items = call.scratch_n<int>((size_t)nh + 1);
-          STAM_CUDA_CHECK(cudaMemcpyAsync(slot_items, slot_first.data(), sizeof(int) * (nh + 1),
-                                          cudaMemcpyHostToDevice, call.stream()));
-          P.nheavy = nh;
-          P.heavy_flag = hflag;
-          auto* d_hf = call.scratch_n<int64_t>((size_t)(2 * nh));
-          heavy_s = call.scratch_n<int64_t>((size_t)nh);
-          d_items = call.scratch_n<HeavyItem>(items.size());
-          hpart = call.scratch_n<double>(items.size() * 32);
-          STAM_CUDA_CHECK(cudaMemcpyAsync(d_hf, hf.data(), sizeof(int64_t) * hf.size(),
-                                          cudaMemcpyHostToDevice, call.stream()));
-          STAM_CUDA_CHECK(cudaMemcpyAsync(heavy_s, hs.data(), sizeof(int64_t) * hs.size(),
-                                          cudaMemcpyHostToDevice, call.stream()));
-          STAM_CUDA_CHECK(cudaMemcpyAsync(d_items, items.data(), sizeof(HeavyItem) * items.size(),
-                                          cudaMemcpyHostToDevice, call.stream()));
-          P.heavy_f = d_hf;
-          // the host vectors must outlive the async copies
-          STAM_CUDA_CHECK(cudaStreamSynchronize(call.stream()));
-          auto* hclaim = static_cast<unsigned long long*>(call.scratch_zero(16));
-          cudaStream_t aux = call.fork();
-          const size_t hsm = sizeof(HeavySmem);
-          STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_dense_heavy_kernel,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
-          call.before_launch("mttkrp_dense_heavy", aux);
-          mttkrp_dense_heavy_kernel<<<(unsigned)std::min<int64_t>((int64_t)items.size(), (int64_t)sms),
-                                      kHvWarps * 32, hsm, aux>>>(P, d_items, (int)items.size(), hclaim,
-                                                                hpart);
-          call.after_launch(aux);
-        }
-      }
-#endif
       call.before_launch(fast ? "mttkrp_dense32" : "mttkrp_dense_generic");
       if (fast)
       {
@@ -1434,13 +1072,6 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
       mttkrp_dense_fixup_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(P.nchunks, 8), (int64_t)sms * 8)),
                                   256, 0, call.stream()>>>(P, L);
       call.after_launch();
-      if (P.nheavy > 0) {
-        call.join();
-        call.before_launch("mttkrp_dense_heavy_reduce");
-        mttkrp_dense_heavy_reduce_kernel<<<(unsigned)P.nheavy, 1024, 0, call.stream()>>>(
-            P, slot_items, hpart, heavy_s);
-        call.after_launch();
-      }
     }
     call.finish_dense_result(A);
     call.finish();
@@ -1451,11 +1082,147 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
   });
 }
 
+namespace stamgpu {
+namespace {
+__global__ void mttkrp_pos_shift_kernel(int64_t* p, int64_t n, int64_t delta) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    p[t] += delta;
+}
+
+// Host CSF input (the e2e case): the CSF is 6.4 GB at config 5 and PCIe H2D
+// (~55 GB/s) bounds the call, so the slices go up in nnz-balanced blocks on
+// the copy stream, all issued at once into full-size device arrays (absolute
+// positions stay valid), each block is evaluated by the device path as soon
+// as its copies land, and its result rows go down on the d2h stream into a
+// pinned host result sized by the bound I x R while later blocks upload.
+int mttkrp_sparse_streamed(stam_cuda_ctx* ctx, const stam_csf3_view* B, const stam_csr_view* Cv,
+                           const stam_csr_view* Dv, const stam_options* opts,
+                           stam_csr_result* A, stam_stats* stats) {
+  return guarded([&] {
+    stam_options o = *opts;
+    o.result_mem = STAM_MEM_DEVICE;
+    o.timing = 0;
+    Call call(reinterpret_cast<Ctx*>(ctx), &o, stats);
+    check_csf3_view(B, "mttkrp B");
+    check_csr_view(Cv, "mttkrp C");
+    check_csr_view(Dv, "mttkrp D");
+    if (Cv->nrows != B->dims[1] || Dv->nrows != B->dims[2])
+      fail(STAM_ERR_DIMENSION_MISMATCH, "mttkrp: C rows != dim 1 or D rows != dim 2");
+    if (Cv->ncols != Dv->ncols) fail(STAM_ERR_DIMENSION_MISMATCH, "mttkrp: C and D ranks differ");
+    const int64_t I = B->dims[0], R = Cv->ncols;
+    auto dev_csr = [&](const stam_csr_view* v) {
+      stam_csr_view d = *v;
+      d.pos = call.device_input(v->pos, (size_t)v->nrows + 1, v->mem);
+      d.idx = call.device_input(v->idx, (size_t)v->nnz, v->mem);
+      d.vals = call.device_input(v->vals, (size_t)v->nnz, v->mem);
+      d.mem = STAM_MEM_DEVICE;
+      return d;
+    };
+    const stam_csr_view Cd = dev_csr(Cv), Dd = dev_csr(Dv);
+    const int64_t* d_pos1 = call.device_input(B->pos1, (size_t)I + 1, B->mem);
+    auto* d_idx1 = call.host_staging<int64_t>((size_t)B->nfibers);
+    auto* d_pos2 = call.host_staging<int64_t>((size_t)B->nfibers + 1);
+    auto* d_idx2 = call.host_staging<int64_t>((size_t)B->nnz);
+    auto* d_vals = call.host_staging<double>((size_t)B->nnz);
+    // nnz-balanced slice blocks (~16M nonzeros each)
+    int64_t nblocks = std::max<int64_t>(2, std::min<int64_t>(64, ceil_div(B->nnz, (int64_t)1 << 24)));
+    nblocks = std::min(nblocks, I);
+    std::vector<int64_t> sb{0};
+    for (int64_t b = 1; b < nblocks; b++) {
+      const int64_t target = B->nnz * b / nblocks;
+      // first slice whose nonzeros start at or after target
+      int64_t lo = sb.back(), hi = I;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (B->pos2[B->pos1[mid]] < target) lo = mid + 1; else hi = mid;
+      }
+      if (lo > sb.back() && lo < I) sb.push_back(lo);
+    }
+    sb.push_back(I);
+    nblocks = (int64_t)sb.size() - 1;
+    std::vector<cudaEvent_t> landed((size_t)nblocks, nullptr);
+    for (int64_t b = 0; b < nblocks; b++) {
+      const int64_t f0 = B->pos1[sb[(size_t)b]], f1 = B->pos1[sb[(size_t)b + 1]];
+      const int64_t z0 = B->pos2[f0], z1 = B->pos2[f1];
+      call.copy_range(d_idx1 + f0, B->idx1 + f0, sizeof(int64_t) * (size_t)(f1 - f0));
+      call.copy_range(d_pos2 + f0, B->pos2 + f0, sizeof(int64_t) * (size_t)(f1 - f0 + 1));
+      call.copy_range(d_idx2 + z0, B->idx2 + z0, sizeof(int64_t) * (size_t)(z1 - z0));
+      call.copy_range(d_vals + z0, B->vals + z0, sizeof(double) * (size_t)(z1 - z0));
+      // own events: the per-block device calls below reuse the context's pool
+      STAM_CUDA_CHECK(cudaEventCreateWithFlags(&landed[(size_t)b], cudaEventDisableTiming));
+      STAM_CUDA_CHECK(cudaEventRecord(landed[(size_t)b], call.ctx()->copy_stream));
+    }
+    struct EventsGuard {
+      std::vector<cudaEvent_t>& ev;
+      ~EventsGuard() {
+        for (auto e : ev)
+          if (e) cudaEventDestroy(e);
+      }
+    } events_guard{landed};
+    call.alloc_csr_result_host(A, I, R, I * R);
+    A->pos[0] = 0;
+    std::vector<stam_csr_result> parts((size_t)nblocks);
+    int64_t off = 0, launches = 0, mults = 0;
+    int status = STAM_OK;
+    const int sms = call.ctx()->num_sms;
+    for (int64_t b = 0; b < nblocks && status == STAM_OK; b++) {
+      const int64_t s0 = sb[(size_t)b], s1 = sb[(size_t)b + 1];
+      call.wait(landed[(size_t)b]);
+      stam_csf3_view Bv = *B;
+      Bv.dims[0] = s1 - s0;
+      Bv.pos1 = d_pos1 + s0;
+      Bv.idx1 = d_idx1;
+      Bv.pos2 = d_pos2;
+      Bv.idx2 = d_idx2;
+      Bv.vals = d_vals;
+      Bv.mem = STAM_MEM_DEVICE;
+      stam_csr_result& Ab = parts[(size_t)b];
+      std::memset(&Ab, 0, sizeof(Ab));
+      stam_stats st{};
+      status = stam_cuda_mttkrp_sparse(ctx, &Bv, &Cd, &Dd, &o, &Ab, &st);
+      if (status != STAM_OK) break;
+      mults += st.mults;
+      launches += st.kernel_launches;
+      mttkrp_pos_shift_kernel<<<(unsigned)std::min<int64_t>(ceil_div(s1 - s0, 256), (int64_t)sms * 4),
+                                256, 0, call.stream()>>>(Ab.pos + 1, s1 - s0, off);
+      STAM_CUDA_CHECK(cudaGetLastError());
+      cudaEvent_t ready = call.event();
+      STAM_CUDA_CHECK(cudaEventRecord(ready, call.stream()));
+      call.d2h_range(A->pos + s0 + 1, Ab.pos + 1, sizeof(int64_t) * (size_t)(s1 - s0), ready);
+      call.d2h_range(A->idx + off, Ab.idx, sizeof(int64_t) * (size_t)Ab.nnz, nullptr);
+      call.d2h_range(A->vals + off, Ab.vals, sizeof(double) * (size_t)Ab.nnz, nullptr);
+      off += Ab.nnz;
+    }
+    call.finish_csr_result_host(A, off);  // joins the downloads
+    for (auto& Ab : parts)
+      if (Ab.handle) stam_cuda_release(ctx, Ab.handle);
+    if (status != STAM_OK) {
+      const std::string msg = stam_cuda_last_error();
+      fail(status, msg);
+    }
+    call.finish();
+    stam_stats* st = call.stats();
+    st->mults = mults;
+    st->adds = mults;
+    st->ws_resets = B->nfibers + I;
+    st->appends = off;
+    st->kernel_launches += launches;
+  });
+}
+}  // namespace
+}  // namespace stamgpu
+
 extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view* B,
                                        const stam_csr_view* Cv, const stam_csr_view* Dv,
                                        const stam_options* opts, stam_csr_result* A,
                                        stam_stats* stats) {
   using namespace stamgpu;
+  if (ctx && B && Cv && Dv && opts && B->mem == STAM_MEM_HOST && opts->result_mem == STAM_MEM_HOST &&
+      B->nnz >= ((int64_t)1 << 24) && B->dims[0] > 1 && Cv->ncols > 0 && Cv->ncols <= 512 &&
+      B->dims[0] * Cv->ncols <= ((int64_t)1 << 29) && B->pos1 && B->pos2 &&
+      std::getenv("STAM_NO_STREAM") == nullptr)
+    return mttkrp_sparse_streamed(ctx, B, Cv, Dv, opts, A, stats);
   return guarded([&] {
     Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
     check_csf3_view(B, "mttkrp B");
@@ -1466,7 +1233,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     if (Cv->ncols != Dv->ncols) fail(STAM_ERR_DIMENSION_MISMATCH, "mttkrp: C and D ranks differ");
     const int64_t I = B->dims[0], R = Cv->ncols;
     const size_t ws_bytes = (((size_t)R * 8 + (size_t)((R + 31) / 32) * 4) + 15) & ~(size_t)15;
-    const size_t smem = ws_bytes * kSpWarps + match_owners_bytes(8) * kSpWarps;
+    const size_t smem = ws_bytes * kSpWarps + match_queue_bytes() * kSpWarps;
     if (smem > call.ctx()->smem_optin)
       fail(STAM_ERR_UNSUPPORTED_MERGE, "sparse mttkrp: rank too large for the shared-memory "
                                        "row workspace in ABI v1 (R <= ~1700)");
@@ -1497,11 +1264,16 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     // factor-row column bitmaps when R fits W <= 8 words
     const int64_t words = (R + 63) / 64;
     const int W = words <= 1 ? 1 : words <= 2 ? 2 : words <= 4 ? 4 : words <= 8 ? 8 : 0;
-    const size_t smem_w = ws_bytes * kSpWarps + match_owners_bytes(W > 0 ? W : 1) * kSpWarps;
+    const size_t smem_w = ws_bytes * kSpWarps + match_queue_bytes() * kSpWarps;
+    // both bitmaps in one block; rows are read with 256-bit loads (W = 4):
+    // 32-byte aligned
+    const size_t bm_words = (size_t)((Cv->nrows + Dv->nrows) * (W > 0 ? W : 1)) + 8;
+    auto* bm_raw = W > 0 ? call.scratch_n<unsigned long long>(bm_words) : nullptr;
+    auto* bm_base = reinterpret_cast<unsigned long long*>(((uintptr_t)bm_raw + 31) & ~(uintptr_t)31);
+    size_t bm_used = 0;
     auto build_bm = [&](const int64_t* pos, const int64_t* idx, int64_t nrows) {
-      // rows are read with 256-bit loads (W = 4): align the array to 32 bytes
-      auto* raw = call.scratch_n<unsigned long long>((size_t)(nrows * W) + 4);
-      auto* bm = reinterpret_cast<unsigned long long*>(((uintptr_t)raw + 31) & ~(uintptr_t)31);
+      unsigned long long* bm = bm_base + bm_used;
+      bm_used += (size_t)(nrows * W);
       const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nrows, 256),
                                                         (int64_t)call.ctx()->num_sms * 8);
       call.before_launch("mttkrp_factor_bitmap");
@@ -1527,7 +1299,14 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps),
                                              (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
       call.before_launch("mttkrp_sparse");
-      kern<<<(unsigned)grid, kSpWarps * 32, smem_w, call.stream()>>>(P);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3(kSpWarps * 32);
+      cfg.dynamicSmemBytes = smem_w;
+      cfg.stream = call.stream();
+      cfg.attrs = nullptr;
+      cfg.numAttrs = 0;
+      STAM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, P));
       call.after_launch();
     };
     switch (W) {

@@ -26,6 +26,7 @@ Call::Call(Ctx* ctx, const stam_options* opts, stam_stats* stats) : ctx_(ctx) {
   std::memset(stats_, 0, sizeof(stam_stats));
   STAM_CUDA_CHECK(cudaSetDevice(ctx_->device));
   ctx_->event_next = 0;
+  ctx_->sync_next = 0;
 }
 
 Call::~Call() {
@@ -104,7 +105,17 @@ const void* Call::stage(const void* p, size_t bytes, int32_t mem) {
   return d;
 }
 
-cudaEvent_t Call::event() { return next_event(); }
+cudaEvent_t Call::event() {
+  // ordering-only events: no timestamps (cheaper to record and wait on)
+  if (ctx_->sync_next >= ctx_->sync_pool.size()) {
+    for (int e = 0; e < 64; e++) {
+      cudaEvent_t ev;
+      STAM_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ctx_->sync_pool.push_back(ev);
+    }
+  }
+  return ctx_->sync_pool[ctx_->sync_next++];
+}
 
 void Call::copy_range(void* dst, const void* src, size_t bytes) {
   if (!ctx_->copy_stream)
@@ -275,6 +286,39 @@ void Call::finish_csr_result_streamed(stam_csr_result* r, int64_t nnz) {
   r->idx = (int64_t*)(h + pos_b);
   r->vals = (double*)(h + pos_b + idx_b);
   r->mem = STAM_MEM_HOST;
+}
+
+void Call::alloc_csr_result_host(stam_csr_result* r, int64_t nrows, int64_t ncols,
+                                 int64_t nnz_capacity) {
+  if (!r) fail(STAM_ERR_PRECONDITION_VIOLATED, "null result");
+  std::memset(r, 0, sizeof(*r));
+  const size_t pos_b = align_up((size_t)(nrows + 1) * sizeof(int64_t), 256);
+  const size_t idx_b = align_up((size_t)std::max<int64_t>(nnz_capacity, 1) * sizeof(int64_t), 256);
+  const size_t val_b = align_up((size_t)std::max<int64_t>(nnz_capacity, 1) * sizeof(double), 256);
+  auto* own = new Owned();
+  char* h = nullptr;
+  try {
+    h = static_cast<char*>(pinned_alloc(pos_b + idx_b + val_b));
+  } catch (...) {
+    delete own;
+    throw;
+  }
+  own->host = h;
+  own->host_bytes = pos_b + idx_b + val_b;
+  r->handle = own;
+  adopt_result(&r->handle);
+  r->nrows = nrows;
+  r->ncols = ncols;
+  r->pos = (int64_t*)h;
+  r->idx = (int64_t*)(h + pos_b);
+  r->vals = (double*)(h + pos_b + idx_b);
+  r->mem = STAM_MEM_HOST;
+}
+
+void Call::finish_csr_result_host(stam_csr_result* r, int64_t nnz) {
+  if (d2h_open_) STAM_CUDA_CHECK(cudaStreamSynchronize(ctx_->d2h_stream));
+  d2h_open_ = false;
+  r->nnz = nnz;
 }
 
 int64_t* Call::marks() {
@@ -525,6 +569,7 @@ int stam_cuda_ctx_destroy(stam_cuda_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& p : ctx->pinned_free) cudaFreeHost(p.first);
     for (auto ev : ctx->event_pool) cudaEventDestroy(ev);
+    for (auto ev : ctx->sync_pool) cudaEventDestroy(ev);
     if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);

@@ -59,8 +59,10 @@ struct Ctx {
   // small pinned scalars for count read-back (grown on demand)
   int64_t* h_scalars = nullptr;
   int h_scalars_cap = 0;
-  std::vector<cudaEvent_t> event_pool;
+  std::vector<cudaEvent_t> event_pool;  // timing-capable (kernel timings, H2D / D2H times)
   size_t event_next = 0;
+  std::vector<cudaEvent_t> sync_pool;   // cudaEventDisableTiming (stream ordering only)
+  size_t sync_next = 0;
 };
 
 // Result ownership record behind stam_*_result.handle.
@@ -136,6 +138,11 @@ class Call {
                                  int64_t nnz_capacity, int64_t** hpos, int64_t** hidx,
                                  double** hvals);
   void d2h_range(void* dst, const void* src, size_t bytes, cudaEvent_t ready);
+  // Host-only CSR result (pinned, capacity nnz_capacity) filled by the caller
+  // with d2h_range; finish_csr_result_host sets nnz after joining the copies.
+  void alloc_csr_result_host(stam_csr_result* r, int64_t nrows, int64_t ncols,
+                             int64_t nnz_capacity);
+  void finish_csr_result_host(stam_csr_result* r, int64_t nnz);
   void finish_csr_result_streamed(stam_csr_result* r, int64_t nnz);
   int64_t* marks();
   void alloc_dense_result(stam_dense_result* r, int64_t nrows, int64_t ncols);

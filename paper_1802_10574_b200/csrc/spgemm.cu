@@ -35,7 +35,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "index.cuh"
@@ -1205,6 +1208,14 @@ __global__ void gather_keys_kernel(const int64_t* rows, int64_t n, const int64_t
   if (t < n) keys[t] = (uint64_t)prod[rows[t]];
 }
 
+// pos[i] - base for a row block (the block's own CSR view) and pos[i] + off
+// for a block result placed after the earlier blocks' entries.
+__global__ void pos_shift_kernel(const int64_t* in, int64_t* out, int64_t n, int64_t delta) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = in[t] + delta;
+}
+
 // ---------------------------------------------------------------------------
 // Narrow B (n <= kNarrowCols columns) with short rows (P_i <= pmax): one fused
 // pass, no symbolic kernel, no bins, no scan.  A warp per row of a tile of
@@ -1222,8 +1233,11 @@ constexpr int kNarrowRows = 8;  // warps (rows) per CTA tile
 constexpr int kNarrowMaxP = 1024;
 
 __global__ void narrow_products_kernel(const SpgemmParams P, unsigned long long* out) {
-  // out[0] += products, out[1] = max products of a row (a warp per row)
+  // out[0] += products, out[1] = max products of a row (a warp per row; one
+  // pair of atomics per CTA)
+  __shared__ unsigned long long s_tot[32], s_max[32];
   const unsigned lane = lane_id();
+  const int wib = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long tot = 0, mx = 0;
@@ -1239,12 +1253,25 @@ __global__ void narrow_products_kernel(const SpgemmParams P, unsigned long long*
     mx = max(mx, s);
   }
   if (lane == 0) {
-    if (tot) atomicAdd(&out[0], tot);
-    atomicMax(&out[1], mx);
+    s_tot[wib] = tot;
+    s_max[wib] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0, m = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      t += s_tot[w];
+      m = max(m, s_max[w]);
+    }
+    if (t) atomicAdd(&out[0], t);
+    atomicMax(&out[1], m);
   }
 }
 
-// Enumerates the row's products 32 at a time: f(col, value) per product.
+// Enumerates the row's products entry by entry (the warp walks the A entries,
+// lanes cover each entry's B row: coalesced reads of the B row, no product ->
+// entry search), two entries per step so two gathers are in flight per lane.
+// f(col, value) sees every product once; kNumeric false skips the values.
 template <bool kNumeric, typename F>
 __device__ __forceinline__ void narrow_products(const SpgemmParams& P, int64_t a0, int64_t a1,
                                                 F f) {
@@ -1260,41 +1287,25 @@ __device__ __forceinline__ void narrow_products(const SpgemmParams& P, int64_t a
       len = (int)(P.bpos[k + 1] - b0);
       if (kNumeric) av = P.avals[p];
     }
-    const int inc = warp_inclusive_scan(len);
-    const int total = __shfl_sync(kFull, inc, 31);
-    const int off = inc - len;  // first product of lane's entry
-    for (int base = 0; base < total; base += 32 * 4) {
-      int64_t q[4];
-      double a[4];
-      bool ok[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int j = base + 32 * u + lane;
-        ok[u] = j < total;
-        // entry holding product j: the last lane whose off <= j
-        int e = 0;
-#pragma unroll
-        for (int st = 16; st >= 1; st >>= 1) {
-          const int ov = __shfl_sync(kFull, off, (e + st) & 31);
-          if (ov <= j) e += st;
-        }
-        // (the last lane with off <= j holds products: empty entries share
-        // their offset with the next nonempty one)
-        const int64_t be = __shfl_sync(kFull, b0, e);
-        const int oe = __shfl_sync(kFull, off, e);
-        a[u] = kNumeric ? __shfl_sync(kFull, av, e) : 0.0;
-        q[u] = be + (j - oe);
+    const int nent = (int)min((int64_t)32, a1 - c);
+    for (int e = 0; e < nent; e += 2) {
+      const int64_t bx = __shfl_sync(kFull, b0, e);
+      const int lx = __shfl_sync(kFull, len, e);
+      const double ax = kNumeric ? __shfl_sync(kFull, av, e) : 0.0;
+      const int e1 = min(e + 1, 31);
+      const int64_t by = __shfl_sync(kFull, b0, e1);
+      const int ly = e + 1 < nent ? __shfl_sync(kFull, len, e1) : 0;
+      const double ay = kNumeric ? __shfl_sync(kFull, av, e1) : 0.0;
+      const int lm = max(lx, ly);
+      for (int t = lane; t < lm; t += 32) {
+        const bool okx = t < lx, oky = t < ly;
+        const int64_t cx = okx ? P.bidx[bx + t] : 0;
+        const int64_t cy = oky ? P.bidx[by + t] : 0;
+        const double vx = (kNumeric && okx) ? P.bvals[bx + t] : 0.0;
+        const double vy = (kNumeric && oky) ? P.bvals[by + t] : 0.0;
+        if (okx) f(cx, kNumeric ? mul_rn(ax, vx) : 0.0);
+        if (oky) f(cy, kNumeric ? mul_rn(ay, vy) : 0.0);
       }
-      int64_t col[4];
-      double bv[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        col[u] = ok[u] ? P.bidx[q[u]] : 0;
-        bv[u] = (kNumeric && ok[u]) ? P.bvals[q[u]] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (ok[u]) f(col[u], kNumeric ? mul_rn(a[u], bv[u]) : 0.0);
     }
   }
 }
@@ -1481,7 +1492,7 @@ bool spgemm_narrow(stamrt::Call& call, const stam_csr_view* A, const stam_csr_vi
   auto* ctl = static_cast<unsigned long long*>(
       call.scratch_zero(sizeof(unsigned long long) * (size_t)(4 + ntiles)));
   call.before_launch("spgemm_narrow_products");
-  narrow_products_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)sms * 8), 256, 0,
+  narrow_products_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)sms * 2), 256, 0,
                            call.stream()>>>(P, ctl);
   call.after_launch();
   int64_t hv[2];
@@ -1525,9 +1536,114 @@ bool spgemm_narrow(stamrt::Call& call, const stam_csr_view* A, const stam_csr_vi
 }  // namespace
 }  // namespace stamgpu
 
+namespace stamgpu {
+namespace {
+// Host result of a large product: row blocks, each computed by the device
+// pipeline into a device result whose rows go down to the pinned host result
+// on the d2h stream while the next block computes (the result is ~16x the
+// inputs at config 3: the PCIe download, not the kernels, bounds the call).
+// Inputs are staged once; block b's pos is rebased on the device.
+int spgemm_streamed(stam_cuda_ctx* ctx, const stam_csr_view* A, const stam_csr_view* B,
+                    const stam_options* opts, stam_csr_result* Cr, stam_stats* stats) {
+  using stamrt::ceil_div;
+  return guarded([&] {
+    stam_options o = *opts;
+    o.result_mem = STAM_MEM_DEVICE;
+    o.timing = 0;
+    Call call(reinterpret_cast<Ctx*>(ctx), &o, stats);
+    const int64_t m = A->nrows, n = B->ncols;
+    SpgemmParams P{};
+    P.m = m;
+    P.apos = call.device_input(A->pos, (size_t)m + 1, A->mem);
+    P.aidx = call.device_input(A->idx, (size_t)A->nnz, A->mem);
+    P.avals = call.device_input(A->vals, (size_t)A->nnz, A->mem);
+    const bool same = B->pos == A->pos && B->idx == A->idx && B->vals == A->vals;
+    P.bpos = same ? P.apos : call.device_input(B->pos, (size_t)B->nrows + 1, B->mem);
+    P.bidx = same ? P.aidx : call.device_input(B->idx, (size_t)B->nnz, B->mem);
+    P.bvals = same ? P.avals : call.device_input(B->vals, (size_t)B->nnz, B->mem);
+    const int sms = call.ctx()->num_sms;
+    auto* ctl = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 2));
+    call.before_launch("spgemm_narrow_products");
+    narrow_products_kernel<<<(unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)sms * 8), 256, 0,
+                             call.stream()>>>(P, ctl);
+    call.after_launch();
+    int64_t hv[2];
+    call.read_scalars(reinterpret_cast<const int64_t*>(ctl), 2, hv);
+    const int64_t products = hv[0];
+    int64_t nblocks = 8;
+    if (const char* e = std::getenv("STAM_SPGEMM_BLOCKS")) nblocks = std::max(1, std::atoi(e));
+    nblocks = std::max<int64_t>(1, std::min<int64_t>(nblocks, m));
+    std::vector<int64_t> rb((size_t)nblocks + 1), eb((size_t)nblocks + 1);
+    for (int64_t b = 0; b <= nblocks; b++) rb[(size_t)b] = m * b / nblocks;
+    // entry offsets of the block boundaries
+    auto* bnd = call.scratch_n<int64_t>((size_t)nblocks + 1);
+    for (int64_t b = 0; b <= nblocks; b++)
+      STAM_CUDA_CHECK(cudaMemcpyAsync(bnd + b, P.apos + rb[(size_t)b], sizeof(int64_t),
+                                      cudaMemcpyDeviceToDevice, call.stream()));
+    call.read_scalars(bnd, (int)nblocks + 1, eb.data());
+    call.alloc_csr_result_host(Cr, m, n, products);
+    Cr->pos[0] = 0;
+    stam_csr_view Bv{B->nrows, B->ncols, B->nnz, P.bpos, P.bidx, P.bvals, STAM_MEM_DEVICE, 0};
+    std::vector<stam_csr_result> parts((size_t)nblocks);
+    int64_t off = 0, launches = 0;
+    stam_stats acc{};
+    int status = STAM_OK;
+    for (int64_t b = 0; b < nblocks && status == STAM_OK; b++) {
+      const int64_t r0 = rb[(size_t)b], r1 = rb[(size_t)b + 1];
+      auto* pb = call.scratch_n<int64_t>((size_t)(r1 - r0) + 1);
+      pos_shift_kernel<<<(unsigned)std::min<int64_t>(ceil_div(r1 - r0 + 1, 256), (int64_t)sms * 4), 256, 0,
+                         call.stream()>>>(P.apos + r0, pb, r1 - r0 + 1, -eb[(size_t)b]);
+      STAM_CUDA_CHECK(cudaGetLastError());
+      stam_csr_view Av{r1 - r0, A->ncols, eb[(size_t)b + 1] - eb[(size_t)b], pb,
+                       P.aidx + eb[(size_t)b], P.avals + eb[(size_t)b], STAM_MEM_DEVICE, 0};
+      stam_stats sb{};
+      stam_csr_result& Cb = parts[(size_t)b];
+      std::memset(&Cb, 0, sizeof(Cb));
+      status = stam_cuda_spgemm(ctx, &Av, &Bv, &o, &Cb, &sb);
+      if (status != STAM_OK) break;
+      acc.mults += sb.mults;
+      acc.ws_inserts += sb.ws_inserts;
+      launches += sb.kernel_launches;
+      // block rows after the earlier blocks' entries, then down to the host
+      pos_shift_kernel<<<(unsigned)std::min<int64_t>(ceil_div(r1 - r0, 256), (int64_t)sms * 4), 256, 0,
+                         call.stream()>>>(Cb.pos + 1, Cb.pos + 1, r1 - r0, off);
+      STAM_CUDA_CHECK(cudaGetLastError());
+      cudaEvent_t ready = call.event();
+      STAM_CUDA_CHECK(cudaEventRecord(ready, call.stream()));
+      call.d2h_range(Cr->pos + r0 + 1, Cb.pos + 1, sizeof(int64_t) * (size_t)(r1 - r0), ready);
+      call.d2h_range(Cr->idx + off, Cb.idx, sizeof(int64_t) * (size_t)Cb.nnz, nullptr);
+      call.d2h_range(Cr->vals + off, Cb.vals, sizeof(double) * (size_t)Cb.nnz, nullptr);
+      off += Cb.nnz;
+    }
+    call.finish_csr_result_host(Cr, off);  // joins the downloads
+    for (auto& Cb : parts)
+      if (Cb.handle) stam_cuda_release(ctx, Cb.handle);
+    if (status != STAM_OK) {
+      const std::string msg = stam_cuda_last_error();
+      fail(status, msg);
+    }
+    call.finish();
+    stam_stats* st = call.stats();
+    st->mults = acc.mults;
+    st->adds = acc.mults;
+    st->ws_inserts = acc.ws_inserts;
+    st->ws_resets = m;
+    st->appends = off;
+    st->kernel_launches += launches;
+  });
+}
+}  // namespace
+}  // namespace stamgpu
+
 extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, const stam_csr_view* B,
                                 const stam_options* opts, stam_csr_result* Cr, stam_stats* stats) {
   using namespace stamgpu;
+  // a host result of a large product streams down block by block
+  if (ctx && A && B && opts && opts->result_mem == STAM_MEM_HOST && opts->mode == STAM_MODE_FUSED &&
+      A->nrows >= 65536 && A->nnz >= ((int64_t)1 << 22) && B->ncols > kNarrowCols &&
+      A->ncols == B->nrows && A->nrows > 0 && B->nrows > 0 && B->ncols < (int64_t)UINT32_MAX &&
+      std::getenv("STAM_NO_STREAM") == nullptr)
+    return spgemm_streamed(ctx, A, B, opts, Cr, stats);
   return guarded([&] {
     Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
     check_csr_view(A, "spgemm A");

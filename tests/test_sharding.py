@@ -170,3 +170,46 @@ def test_csf_fibers_partial_slices_sum_to_the_whole():
             if sub.dims[0]:
                 A[s0:s0 + sub.dims[0]] += oracle.mttkrp_dense(sub, Cv, Dv)["vals"]
         assert np.all(np.abs(A - ref["vals"]) <= 1e-12 * np.maximum(np.abs(ref["vals"]), ref["abs"]))
+
+
+def _worker_dense3(rank, world, port, q):
+    """Dense MTTKRP over 3 ranks whose fiber blocks cut the heaviest slice:
+    the boundary-row all-gather completes every cut slice (one slice spans
+    all three blocks here)."""
+    import torch.distributed as dist
+
+    import oracle
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B = None
+        if rank == 0:
+            sizes = np.array([3000, 10, 10, 5, 5, 3, 2, 1], dtype=np.int64)  # one dominant slice
+            B = G.csf3((8, 60, 80), sizes, 91)
+            Cm, Dm = G.dense(60, 8, 92).vals, G.dense(80, 8, 93).vals
+        A = S.distributed_mttkrp_dense(B, Cm if rank == 0 else None, Dm if rank == 0 else None,
+                                       lambda b, c, d: oracle.mttkrp_dense(b, c, d)["vals"])
+        if rank == 0:
+            fb = S.fiber_bounds(B, world)
+            spans = [S.csf_fibers(B, int(fb[r]), int(fb[r + 1]))[0] for r in range(world)]
+            r = oracle.mttkrp_dense(B, Cm, Dm)
+            ok = bool(np.all(np.abs(A - r["vals"]) <= 1e-12 * np.maximum(np.abs(r["vals"]), r["abs"])))
+            q.put({"ok": ok, "all_start_in_slice0": spans == [0, 0, 0]})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_mttkrp_dense_slice_spanning_three_ranks_gloo():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dense3, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = q.get(timeout=5)
+    assert res == {"ok": True, "all_start_in_slice0": True}, res
