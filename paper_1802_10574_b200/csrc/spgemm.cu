@@ -95,6 +95,7 @@ struct SpgemmParams {
   const int64_t* bpos;
   const int64_t* bidx;
   const double* bvals;
+  const uint32_t* bcol32;    // B's column indices as u32 (n < 2^32): half the gather bytes
   int64_t* prod;             // [m] products per row
   uint2* span;               // [m] first/last column any of the row's B rows holds (x > y: none)
   uint2* bspan;              // [nrows(B)] first/last column of each B row (x > y: empty)
@@ -260,6 +261,14 @@ __global__ void bspan_kernel(const SpgemmParams P, int64_t nb) {
   }
 }
 
+// B's int64 column indices as u32 for the product gathers (4 instead of 8
+// bytes per product in both passes; 16M entries at config 3: ~30 us).
+__global__ void bcol32_kernel(const int64_t* bidx, int64_t nnz, uint32_t* out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (uint32_t)__ldcs(bidx + t);
+}
+
 // Rows with more than kLongA entries: a warp per row, claimed dynamically.
 __global__ void rowprod_long_kernel(const SpgemmParams P) {
   __shared__ unsigned long long hist[kNumBins];
@@ -373,7 +382,7 @@ __device__ __forceinline__ void tiny_product(const SpgemmParams& P, int64_t i, b
   if (g >= prod) return;
   const int p = entry_of(P.aoff + a0, na, g);
   const int64_t q = P.bst[a0 + p] + (g - P.aoff[a0 + p]);
-  col = P.bidx[q];
+  col = P.bcol32[q];
   if (numeric) val = mul_rn(P.avals[a0 + p], P.bvals[q]);
   has = true;
 }
@@ -522,7 +531,7 @@ __device__ __forceinline__ void for_products(const SpgemmParams& P, int64_t a0, 
       col[u] = 0;
       bv[u] = 0.0;
       if (ok[u]) {
-        col[u] = P.bidx[q[u]];
+        col[u] = P.bcol32[q[u]];
         if (kNumeric) bv[u] = P.bvals[q[u]];
       }
     }
@@ -1429,6 +1438,14 @@ void prepare(stamrt::Call& call, const stam_csr_view* A, const stam_csr_view* B,
   P.arows = call.scratch_n<int64_t>((size_t)std::max<int64_t>(m, 1));
   P.narows = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 2));
   const int sms = call.ctx()->num_sms;
+  {
+    auto* c32 = call.scratch_n<uint32_t>((size_t)std::max<int64_t>(B->nnz, 1));
+    call.before_launch("spgemm_bcol32");
+    bcol32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(std::max<int64_t>(B->nnz, 1), 256), (int64_t)sms * 16), 256, 0,
+                    call.stream()>>>(P.bidx, B->nnz, c32);
+    call.after_launch();
+    P.bcol32 = c32;
+  }
   call.before_launch("spgemm_bspan");
   bspan_kernel<<<(unsigned)std::min<int64_t>(ceil_div(B->nrows, 256), (int64_t)sms * 8), 256, 0,
                  call.stream()>>>(P, B->nrows);
