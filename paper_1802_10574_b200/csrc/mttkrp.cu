@@ -1084,6 +1084,13 @@ extern "C" int stam_cuda_mttkrp_dense(stam_cuda_ctx* ctx, const stam_csf3_view* 
 
 namespace stamgpu {
 namespace {
+// staging budget of the sparse path (bytes): see mttkrp_sparse_blocked
+int64_t sparse_stage_budget() {
+  int64_t mb = 4096;
+  if (const char* e = std::getenv("STAM_SPARSE_STAGE_MB")) mb = std::max(1, std::atoi(e));
+  return mb << 20;
+}
+
 __global__ void mttkrp_pos_shift_kernel(int64_t* p, int64_t n, int64_t delta) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x)
@@ -1127,6 +1134,7 @@ int mttkrp_sparse_streamed(stam_cuda_ctx* ctx, const stam_csf3_view* B, const st
     auto* d_vals = call.host_staging<double>((size_t)B->nnz);
     // nnz-balanced slice blocks (~16M nonzeros each)
     int64_t nblocks = std::max<int64_t>(2, std::min<int64_t>(64, ceil_div(B->nnz, (int64_t)1 << 24)));
+    nblocks = std::max(nblocks, ceil_div(I * R * 16, sparse_stage_budget()));
     nblocks = std::min(nblocks, I);
     std::vector<int64_t> sb{0};
     for (int64_t b = 1; b < nblocks; b++) {
@@ -1210,6 +1218,95 @@ int mttkrp_sparse_streamed(stam_cuda_ctx* ctx, const stam_csf3_view* B, const st
     st->kernel_launches += launches;
   });
 }
+// Bounded staging (ADVICE: the fixed-stride staging is 16·I·R bytes whatever
+// the output's sparsity, 2 GB at config 5): when it would exceed the budget
+// (STAM_SPARSE_STAGE_MB, default 4096), slices are evaluated in blocks whose
+// staging fits, each by the device path, and the block results are placed
+// into one exact CSR (device-to-device copies).
+int mttkrp_sparse_blocked(stam_cuda_ctx* ctx, const stam_csf3_view* B, const stam_csr_view* Cv,
+                          const stam_csr_view* Dv, const stam_options* opts, stam_csr_result* A,
+                          stam_stats* stats) {
+  return guarded([&] {
+    stam_options o = *opts;
+    o.result_mem = STAM_MEM_DEVICE;
+    o.timing = 0;
+    Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
+    check_csf3_view(B, "mttkrp B");
+    check_csr_view(Cv, "mttkrp C");
+    check_csr_view(Dv, "mttkrp D");
+    const int64_t I = B->dims[0], R = Cv->ncols;
+    auto dev_csr = [&](const stam_csr_view* v) {
+      stam_csr_view d = *v;
+      d.pos = call.device_input(v->pos, (size_t)v->nrows + 1, v->mem);
+      d.idx = call.device_input(v->idx, (size_t)v->nnz, v->mem);
+      d.vals = call.device_input(v->vals, (size_t)v->nnz, v->mem);
+      d.mem = STAM_MEM_DEVICE;
+      return d;
+    };
+    const stam_csr_view Cd = dev_csr(Cv), Dd = dev_csr(Dv);
+    stam_csf3_view Bd = *B;
+    Bd.pos1 = call.device_input(B->pos1, (size_t)I + 1, B->mem);
+    Bd.idx1 = call.device_input(B->idx1, (size_t)B->nfibers, B->mem);
+    Bd.pos2 = call.device_input(B->pos2, (size_t)B->nfibers + 1, B->mem);
+    Bd.idx2 = call.device_input(B->idx2, (size_t)B->nnz, B->mem);
+    Bd.vals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
+    Bd.mem = STAM_MEM_DEVICE;
+    const int64_t per = std::max<int64_t>(1, sparse_stage_budget() / (16 * R));  // slices per block
+    const int64_t nblocks = ceil_div(I, per);
+    std::vector<stam_csr_result> parts((size_t)nblocks);
+    int64_t total = 0, launches = 0, mults = 0;
+    int status = STAM_OK;
+    for (int64_t b = 0; b < nblocks && status == STAM_OK; b++) {
+      const int64_t s0 = b * per, s1 = std::min(I, s0 + per);
+      stam_csf3_view Bv = Bd;
+      Bv.dims[0] = s1 - s0;
+      Bv.pos1 = Bd.pos1 + s0;
+      stam_csr_result& Ab = parts[(size_t)b];
+      std::memset(&Ab, 0, sizeof(Ab));
+      stam_stats st{};
+      status = stam_cuda_mttkrp_sparse(ctx, &Bv, &Cd, &Dd, &o, &Ab, &st);
+      total += Ab.nnz;
+      mults += st.mults;
+      launches += st.kernel_launches;
+    }
+    if (status == STAM_OK) {
+      call.alloc_csr_result(A, I, R, total);
+      STAM_CUDA_CHECK(cudaMemsetAsync(A->pos, 0, sizeof(int64_t), call.stream()));
+      int64_t off = 0;
+      const int sms = call.ctx()->num_sms;
+      for (int64_t b = 0; b < nblocks; b++) {
+        const int64_t s0 = b * per, s1 = std::min(I, s0 + per);
+        const stam_csr_result& Ab = parts[(size_t)b];
+        STAM_CUDA_CHECK(cudaMemcpyAsync(A->pos + s0 + 1, Ab.pos + 1, sizeof(int64_t) * (size_t)(s1 - s0),
+                                        cudaMemcpyDeviceToDevice, call.stream()));
+        mttkrp_pos_shift_kernel<<<(unsigned)std::min<int64_t>(ceil_div(s1 - s0, 256), (int64_t)sms * 4),
+                                  256, 0, call.stream()>>>(A->pos + s0 + 1, s1 - s0, off);
+        STAM_CUDA_CHECK(cudaGetLastError());
+        STAM_CUDA_CHECK(cudaMemcpyAsync(A->idx + off, Ab.idx, sizeof(int64_t) * (size_t)Ab.nnz,
+                                        cudaMemcpyDeviceToDevice, call.stream()));
+        STAM_CUDA_CHECK(cudaMemcpyAsync(A->vals + off, Ab.vals, sizeof(double) * (size_t)Ab.nnz,
+                                        cudaMemcpyDeviceToDevice, call.stream()));
+        off += Ab.nnz;
+      }
+    }
+    STAM_CUDA_CHECK(cudaStreamSynchronize(call.stream()));
+    for (auto& Ab : parts)
+      if (Ab.handle) stam_cuda_release(ctx, Ab.handle);
+    if (status != STAM_OK) {
+      const std::string msg = stam_cuda_last_error();
+      fail(status, msg);
+    }
+    call.finish_csr_result(A, total);
+    call.finish();
+    stam_stats* st = call.stats();
+    st->mults = mults;
+    st->adds = mults;
+    st->ws_resets = B->nfibers + I;
+    st->appends = total;
+    st->kernel_launches += launches;
+  });
+}
+
 }  // namespace
 }  // namespace stamgpu
 
@@ -1223,6 +1320,9 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       B->dims[0] * Cv->ncols <= ((int64_t)1 << 29) && B->pos1 && B->pos2 &&
       std::getenv("STAM_NO_STREAM") == nullptr)
     return mttkrp_sparse_streamed(ctx, B, Cv, Dv, opts, A, stats);
+  if (ctx && B && Cv && Dv && opts && B->dims[0] > 1 && Cv->ncols > 0 &&
+      B->dims[0] * Cv->ncols * 16 > sparse_stage_budget())
+    return mttkrp_sparse_blocked(ctx, B, Cv, Dv, opts, A, stats);
   return guarded([&] {
     Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
     check_csf3_view(B, "mttkrp B");

@@ -38,3 +38,19 @@ def test_mttkrp_sparse_host_inputs_stream_slice_blocks(ctx):
     # the SPEC counter is the sum over blocks
     dev = ctx.mttkrp(B.to("cuda"), cfg["C"].to("cuda"), cfg["D"].to("cuda"))
     assert dev.nnz == A.nnz
+
+
+def test_mttkrp_sparse_bounded_staging_blocks(ctx, monkeypatch):
+    """A staging budget below 16·I·R bytes splits the slices into blocks whose
+    results are placed into one exact CSR (ADVICE: bounded staging memory)."""
+    cfg = G.make_config(5, scale=0.01)  # 5k slices, R = 256: 20 MB of staging unblocked
+    monkeypatch.setenv("STAM_SPARSE_STAGE_MB", "2")  # -> 512 slices per block
+    st = N.Stats()
+    A = ctx.mttkrp(cfg["B"].to("cuda"), cfg["C"].to("cuda"), cfg["D"].to("cuda"), stats=st)
+    ref = oracle.mttkrp_sparse(cfg["B"], cfg["C"], cfg["D"], nthreads=NT)
+    oracle.compare_csr(A, ref)
+    monkeypatch.delenv("STAM_SPARSE_STAGE_MB")
+    st1 = N.Stats()
+    A1 = ctx.mttkrp(cfg["B"].to("cuda"), cfg["C"].to("cuda"), cfg["D"].to("cuda"), stats=st1)
+    assert A1.nnz == A.nnz and st.mults == st1.mults
+    assert st.kernel_launches > st1.kernel_launches  # ten blocks, each a device call
