@@ -595,6 +595,13 @@ struct SparseParams {
   // column bitmaps of the factor rows (kBmWords 64-bit words per row; R <= 64*W)
   const unsigned long long* cbm;
   const unsigned long long* dbm;
+  // three-phase path: match records per slice (in the slice's staging row)
+  int32_t* rec_cnt;            // [I] records of each slice, -1: overflowed
+  int32_t rec_cap;             // records a staging row holds
+  const int64_t* slice_list;   // slices to evaluate (fallback pass), or null: all
+  int64_t nlist;
+  unsigned long long* ovf;     // [0] overflowed slices (appended to ovf_list)
+  int64_t* ovf_list;
 };
 
 __device__ __forceinline__ int64_t locate(const int64_t* a, int64_t n, int64_t x) {
@@ -929,7 +936,12 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
     int64_t i = 0;
     if (lane == 0) i = (int64_t)atomicAdd(P.tile_counter, 1ull);
     i = __shfl_sync(kFull, i, 0);
-    if (i >= P.I) break;
+    if (P.slice_list) {
+      if (i >= P.nlist) break;
+      i = P.slice_list[i];
+    } else if (i >= P.I) {
+      break;
+    }
     for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
     for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
     __syncwarp();
@@ -957,7 +969,229 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
     __syncwarp();
   }
   mults = warp_sum(mults);
+  if (lane == 0 && mults && P.mults) atomicAdd(P.mults, mults);
+}
+
+// ---------------------------------------------------------------------------
+// Three phases, each with a gathered set below the L2's ~64-80 MB random-
+// gather capacity (profiles/r02/l2_capacity.md; one pass gathers ~104 MB at
+// config 5 and misses on 23-63 % of lookups):
+//  1. match: the CSF streamed once; per fiber the two factor bitmaps and, at
+//     matches, the two row starts (gathered set: 32 + 8 MB).  Each match
+//     becomes a record (C value position, D value position, column, b) in the
+//     slice's own staging row (SoA, rec_cap records); a slice with more
+//     matches than that is listed for the single-pass kernel.
+//  2. D values: every record's b becomes w0 = 0 + b·D(k,r) (32 MB).
+//  3. C values: a warp per slice adds w0·C(j,r) into its R-wide workspace and
+//     drains it sorted over the records it just consumed (32 MB).
+// Same arithmetic and per-entry order as sparse_slice_bm (w0 rounded, then
+// w1(r) += w0·C(j,r)); multi-nonzero fibers finish w0 in phase 1 (their
+// records carry D position -1).
+struct RecRow {
+  int32_t* ci;
+  int32_t* di;
+  uint16_t* r;
+  double* b;
+};
+__device__ __forceinline__ RecRow rec_row(const SparseParams& P, int64_t i) {
+  RecRow x;
+  char* base = reinterpret_cast<char*>(P.stage_idx + i * P.R);
+  x.ci = reinterpret_cast<int32_t*>(base);
+  x.di = x.ci + P.rec_cap;
+  x.r = reinterpret_cast<uint16_t*>(x.di + P.rec_cap);
+  x.b = P.stage_vals + i * P.R;
+  return x;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_match_kernel(const SparseParams P) {
+  const int lane = (int)lane_id();
+  const uint64_t keep = l2_evict_last_policy();
+  unsigned long long mults = 0;
+  while (true) {
+    int64_t i = 0;
+    if (lane == 0) i = (int64_t)atomicAdd(P.tile_counter, 1ull);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= P.I) break;
+    const RecRow rr = rec_row(P, i);
+    const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
+    int nrec = 0;  // warp-uniform
+    bool ovf = false;
+    for (int64_t fb = f0; fb < f1; fb += 32) {
+      const int64_t f = fb + lane;
+      int nm = 0;
+      int64_t j = 0, k = 0;
+      double b = 0.0;
+      unsigned long long bc[W], bd[W];
+#pragma unroll
+      for (int w = 0; w < W; w++) bc[w] = bd[w] = 0ull;
+      bool single = false, general = false;
+      int64_t z0 = 0, z1 = 0;
+      if (f < f1) {
+        j = __ldcs(P.idx1 + f);
+        z0 = __ldcs(P.pos2 + f);
+        z1 = __ldcs(P.pos2 + f + 1);
+        load_bm_keep<W>(P.cbm + j * W, keep, bc);
+        if (z1 - z0 == 1) {
+          single = true;
+          k = __ldcs(P.idx2 + z0);
+          b = __ldcs(P.vals + z0);
+          load_bm_keep<W>(P.dbm + k * W, keep, bd);
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            mults += (unsigned long long)__popcll(bd[w]);
+            nm += __popcll(bc[w] & bd[w]);
+          }
+        } else if (z1 > z0) {
+          general = true;
+          // records for the columns of C_j present in some D_k of the fiber
+          unsigned long long any[W];
+#pragma unroll
+          for (int w = 0; w < W; w++) any[w] = 0ull;
+          for (int64_t z = z0; z < z1; z++) {
+            unsigned long long bz[W];
+            load_bm<W>(P.dbm + P.idx2[z] * W, bz);
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+              mults += (unsigned long long)__popcll(bz[w]);
+              any[w] |= bz[w];
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            bd[w] = any[w];  // the union, for the match count
+            nm += __popcll(bc[w] & any[w]);
+          }
+        }
+      }
+      const int inc = warp_inclusive_scan(nm);
+      const int tot = __shfl_sync(kFull, inc, 31);
+      if (tot == 0) continue;
+      mults += (unsigned long long)nm;
+      if (ovf || nrec + tot > P.rec_cap) {
+        ovf = true;  // the slice goes to the single-pass kernel
+        continue;
+      }
+      if (nm > 0) {
+        int slot = nrec + inc - nm;
+        const int64_t c0 = ld_val(P.cpos + j, keep);
+        if (single) {
+          const int64_t d0 = ld_val(P.dpos + k, keep);
+          int rc = 0, rd = 0;
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            unsigned long long mm = bc[w] & bd[w];
+            while (mm) {
+              const int bit = __ffsll((long long)mm) - 1;
+              const unsigned long long below = (1ull << bit) - 1ull;
+              rr.ci[slot] = (int32_t)(c0 + rc + __popcll(bc[w] & below));
+              rr.di[slot] = (int32_t)(d0 + rd + __popcll(bd[w] & below));
+              rr.r[slot] = (uint16_t)(w * 64 + bit);
+              rr.b[slot] = b;
+              slot++;
+              mm &= mm - 1ull;
+            }
+            rc += __popcll(bc[w]);
+            rd += __popcll(bd[w]);
+          }
+        } else if (general) {
+          int ic = 0;
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            unsigned long long cm = bc[w];
+            while (cm) {
+              const int bit = __ffsll((long long)cm) - 1;
+              if ((bd[w] >> bit) & 1ull) {
+                const int r = w * 64 + bit;
+                double w0 = 0.0;
+                for (int64_t z = z0; z < z1; z++) {
+                  const int64_t kz = P.idx2[z];
+                  unsigned long long bz[W];
+                  load_bm<W>(P.dbm + kz * W, bz);
+                  if ((bz[w] >> bit) & 1ull)
+                    w0 = add_rn(w0, mul_rn(P.vals[z], P.dvals[P.dpos[kz] + bm_rank<W>(bz, r)]));
+                }
+                rr.ci[slot] = (int32_t)(c0 + ic);
+                rr.di[slot] = -1;  // w0 is final
+                rr.r[slot] = (uint16_t)r;
+                rr.b[slot] = w0;
+                slot++;
+              }
+              ic++;
+              cm &= cm - 1ull;
+            }
+          }
+        }
+      }
+      nrec += tot;
+    }
+    if (lane == 0) {
+      P.rec_cnt[i] = ovf ? -1 : nrec;
+      if (ovf) P.ovf_list[atomicAdd(P.ovf, 1ull)] = i;
+    }
+  }
+  mults = warp_sum(mults);
   if (lane == 0 && mults) atomicAdd(P.mults, mults);
+}
+
+// Phase 2: w0 = 0 + b·D(k,r) in place (a warp per slice, lanes over records).
+__global__ void mttkrp_sparse_dvals_kernel(const SparseParams P) {
+  const int lane = (int)lane_id();
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < P.I; i += nwarps) {
+    const int n = P.rec_cnt[i];
+    if (n <= 0) continue;
+    const RecRow rr = rec_row(P, i);
+    for (int t = lane; t < n; t += 32) {
+      const int32_t di = rr.di[t];
+      if (di >= 0) rr.b[t] = add_rn(0.0, mul_rn(rr.b[t], __ldg(P.dvals + di)));
+    }
+  }
+}
+
+// Phase 3: w1(r) += w0·C(j,r) into the warp's workspace, then the sorted
+// drain into the same staging row (its records are consumed by then).
+__global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(const SparseParams P) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = (int)lane_id();
+  const int warp = threadIdx.x >> 5;
+  const int64_t R = P.R;
+  const int nwords = (int)((R + 31) / 32);
+  const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
+  double* wv = reinterpret_cast<double*>(smem_raw + (size_t)warp * ws_bytes);
+  uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < P.I; i += nwarps) {
+    const int n = P.rec_cnt[i];
+    if (n < 0) continue;  // evaluated by the single-pass kernel
+    for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
+    for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
+    __syncwarp();
+    const RecRow rr = rec_row(P, i);
+    for (int t = lane; t < n; t += 32) {
+      const double w0 = rr.b[t];
+      ws_add(wv, wb, rr.r[t], mul_rn(w0, __ldg(P.cvals + rr.ci[t])));
+    }
+    __syncwarp();
+    int64_t* oi = P.stage_idx + i * R;
+    double* ov = P.stage_vals + i * R;
+    int out = 0;
+    for (int w = 0; w < nwords; w++) {
+      const uint32_t bits = wb[w];
+      if (bits == 0) continue;
+      if ((bits >> lane) & 1u) {
+        const int rank = __popc(bits & ((1u << lane) - 1u));
+        const int64_t r = (int64_t)w * 32 + lane;
+        __stcs(reinterpret_cast<long long*>(oi) + out + rank, (long long)r);
+        __stcs(ov + out + rank, wv[r]);
+      }
+      out += __popc(bits);
+    }
+    if (lane == 0) P.out_pos[i + 1] = out;
+    __syncwarp();
+  }
 }
 
 // Copies staged rows (stride R) into the compact CSR: a warp per row.
@@ -1409,12 +1643,73 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       STAM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, P));
       call.after_launch();
     };
-    switch (W) {
-      case 1: launch(mttkrp_sparse_kernel<1>); break;
-      case 2: launch(mttkrp_sparse_kernel<2>); break;
-      case 4: launch(mttkrp_sparse_kernel<4>); break;
-      case 8: launch(mttkrp_sparse_kernel<8>); break;
-      default: launch(mttkrp_sparse_kernel<0>); break;
+    auto launch_single = [&]() {
+      switch (W) {
+        case 1: launch(mttkrp_sparse_kernel<1>); break;
+        case 2: launch(mttkrp_sparse_kernel<2>); break;
+        case 4: launch(mttkrp_sparse_kernel<4>); break;
+        case 8: launch(mttkrp_sparse_kernel<8>); break;
+        default: launch(mttkrp_sparse_kernel<0>); break;
+      }
+    };
+    // three phases (match records, D values, C values + drain) when positions
+    // fit int32 and a staging row holds a useful number of records
+    const int rec_cap = (int)((8 * R) / 10) & ~7;
+    const char* tp = std::getenv("STAM_SP_PHASES");
+    const bool three = W > 0 && Cv->nnz < INT32_MAX && Dv->nnz < INT32_MAX && R <= 65535 &&
+                       rec_cap >= 32 && !(tp && std::atoi(tp) == 1);
+    if (!three) {
+      launch_single();
+    } else {
+      P.rec_cap = rec_cap;
+      P.rec_cnt = call.scratch_n<int32_t>((size_t)I);
+      P.ovf = reinterpret_cast<unsigned long long*>(ctl + 2);
+      P.ovf_list = call.scratch_n<int64_t>((size_t)I);
+      const int sms = call.ctx()->num_sms;
+      auto match = [&](auto kern) {
+        int per_sm = 1;
+        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32, 0));
+        const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
+        call.before_launch("mttkrp_sparse_match");
+        kern<<<(unsigned)grid, kSpWarps * 32, 0, call.stream()>>>(P);
+        call.after_launch();
+      };
+      switch (W) {
+        case 1: match(mttkrp_sparse_match_kernel<1>); break;
+        case 2: match(mttkrp_sparse_match_kernel<2>); break;
+        case 4: match(mttkrp_sparse_match_kernel<4>); break;
+        default: match(mttkrp_sparse_match_kernel<8>); break;
+      }
+      call.before_launch("mttkrp_sparse_dvals");
+      mttkrp_sparse_dvals_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 8), (int64_t)sms * 16), 256, 0,
+                                   call.stream()>>>(P);
+      call.after_launch();
+      {
+        const size_t asmem = ws_bytes * kSpWarps;
+        STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_accum_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+        int per_sm = 1;
+        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mttkrp_sparse_accum_kernel,
+                                                                      kSpWarps * 32, asmem));
+        const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
+        call.before_launch("mttkrp_sparse_accum");
+        mttkrp_sparse_accum_kernel<<<(unsigned)grid, kSpWarps * 32, asmem, call.stream()>>>(P);
+        call.after_launch();
+      }
+      // slices with more matches than a staging row holds: the single pass
+      int64_t nov = 0;
+      call.read_scalars(reinterpret_cast<const int64_t*>(ctl + 2), 1, &nov);
+      if (nov > 0) {
+        SparseParams Q = P;
+        Q.slice_list = P.ovf_list;
+        Q.nlist = nov;
+        Q.mults = nullptr;  // counted by the match phase
+        STAM_CUDA_CHECK(cudaMemsetAsync(P.tile_counter, 0, sizeof(unsigned long long), call.stream()));
+        const SparseParams saved = P;
+        P = Q;
+        launch_single();
+        P = saved;
+      }
     }
     size_t temp_bytes = 0;
     STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, cpos + 1, cpos + 1, I,
