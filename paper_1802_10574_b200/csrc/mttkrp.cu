@@ -590,8 +590,7 @@ struct SparseParams {
   unsigned long long* tile_counter;
   int64_t* total_nnz;
   unsigned long long* mults;  // SPEC counter: |D_k| per nonzero + consumed w0 entries
-  int64_t* stage_idx;         // [I*R] drained rows at a fixed stride
-  double* stage_vals;
+  int64_t* stage;             // [I*2R] per slice: R drained coordinates, then R values
   // column bitmaps of the factor rows (kBmWords 64-bit words per row; R <= 64*W)
   const unsigned long long* cbm;
   const unsigned long long* dbm;
@@ -600,9 +599,18 @@ struct SparseParams {
   int32_t rec_cap;             // records a staging row holds
   const int64_t* slice_list;   // slices to evaluate (fallback pass), or null: all
   int64_t nlist;
+  const unsigned long long* nlist_dev;  // list length on the device (overrides nlist)
   unsigned long long* ovf;     // [0] overflowed slices (appended to ovf_list)
   int64_t* ovf_list;
+  int tma_ok;                  // the CSF arrays sit on 16-byte boundaries (bulk copies)
 };
+
+__device__ __forceinline__ int64_t* stage_idx_row(const SparseParams& P, int64_t i) {
+  return P.stage + i * 2 * P.R;
+}
+__device__ __forceinline__ double* stage_vals_row(const SparseParams& P, int64_t i) {
+  return reinterpret_cast<double*>(P.stage + i * 2 * P.R + P.R);
+}
 
 __device__ __forceinline__ int64_t locate(const int64_t* a, int64_t n, int64_t x) {
   int64_t lo = 0, len = n;
@@ -937,7 +945,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
     if (lane == 0) i = (int64_t)atomicAdd(P.tile_counter, 1ull);
     i = __shfl_sync(kFull, i, 0);
     if (P.slice_list) {
-      if (i >= P.nlist) break;
+      if (i >= (P.nlist_dev ? (int64_t)*P.nlist_dev : P.nlist)) break;
       i = P.slice_list[i];
     } else if (i >= P.I) {
       break;
@@ -951,8 +959,8 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
       sparse_slice(P, i, wv, wb, mults);
     __syncwarp();
     // sorted drain by ballot/popcount over the presence bitmap
-    int64_t* oi = P.stage_idx + i * R;
-    double* ov = P.stage_vals + i * R;
+    int64_t* oi = stage_idx_row(P, i);
+    double* ov = stage_vals_row(P, i);
     int out = 0;
     for (int w = 0; w < nwords; w++) {
       const uint32_t bits = wb[w];
@@ -976,182 +984,363 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
 // Three phases, each with a gathered set below the L2's ~64-80 MB random-
 // gather capacity (profiles/r02/l2_capacity.md; one pass gathers ~104 MB at
 // config 5 and misses on 23-63 % of lookups):
-//  1. match: the CSF streamed once; per fiber the two factor bitmaps and, at
-//     matches, the two row starts (gathered set: 32 + 8 MB).  Each match
-//     becomes a record (C value position, D value position, column, b) in the
-//     slice's own staging row (SoA, rec_cap records); a slice with more
-//     matches than that is listed for the single-pass kernel.
-//  2. D values: every record's b becomes w0 = 0 + b·D(k,r) (32 MB).
-//  3. C values: a warp per slice adds w0·C(j,r) into its R-wide workspace and
-//     drains it sorted over the records it just consumed (32 MB).
-// Same arithmetic and per-entry order as sparse_slice_bm (w0 rounded, then
-// w1(r) += w0·C(j,r)); multi-nonzero fibers finish w0 in phase 1 (their
-// records carry D position -1).
+//  1. match: the CSF streamed once through per-warp shared-memory rings
+//     filled by TMA bulk copies (fiber metadata kMD1 chunks ahead, a chunk's
+//     nonzeros as soon as its pos2 range has landed), so the only loads a lane
+//     waits for are the two factor-row bitmaps (gathered set: 32 MB).  Each
+//     matching (nonzero, column) pair becomes a record (j, k, b | column) in
+//     the slice's own staging row; a slice with more records than the row
+//     holds is listed for the single-pass kernel (which drains into the same
+//     staging row; a placement kernel copies those rows after the scan).
+//  2. D values: every record's b becomes b·D(k,r) (gathered: D's bitmaps, row
+//     starts and values, 52 MB); the slice's distinct columns are counted, so
+//     the row pointers can be scanned before any row is written.
+//  3. C values: a warp per slice adds w0·C(j,r) into its R-wide workspace
+//     (C's bitmaps, row starts and values) and drains it sorted straight into
+//     the CSR.
+// Same arithmetic and per-entry order as sparse_slice_bm: w0(r) = 0 + b·D(k,r)
+// (+ the fiber's further nonzeros in order: their records follow the first
+// one of the column, unflagged), then w1(r) += w0(r)·C(j,r).
+template <int W>
+struct Bm {
+  unsigned long long w[W];
+};
+
+struct __align__(16) MatchRec {
+  int j, k;
+  double b;
+};
+constexpr unsigned kRecFirst = 0x8000u;  // first record of its (fiber, column)
 struct RecRow {
-  int32_t* ci;
-  int32_t* di;
-  uint16_t* r;
-  double* b;
+  MatchRec* rec;
+  uint16_t* col;  // column | kRecFirst
 };
 __device__ __forceinline__ RecRow rec_row(const SparseParams& P, int64_t i) {
   RecRow x;
-  char* base = reinterpret_cast<char*>(P.stage_idx + i * P.R);
-  x.ci = reinterpret_cast<int32_t*>(base);
-  x.di = x.ci + P.rec_cap;
-  x.r = reinterpret_cast<uint16_t*>(x.di + P.rec_cap);
-  x.b = P.stage_vals + i * P.R;
+  x.rec = reinterpret_cast<MatchRec*>(P.stage + i * 2 * P.R);
+  x.col = reinterpret_cast<uint16_t*>(x.rec + P.rec_cap);
   return x;
 }
 
-template <int W>
-__global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_match_kernel(const SparseParams P) {
-  const int lane = (int)lane_id();
-  const uint64_t keep = l2_evict_last_policy();
-  unsigned long long mults = 0;
-  while (true) {
-    int64_t i = 0;
-    if (lane == 0) i = (int64_t)atomicAdd(P.tile_counter, 1ull);
-    i = __shfl_sync(kFull, i, 0);
-    if (i >= P.I) break;
-    const RecRow rr = rec_row(P, i);
-    const int64_t f0 = P.pos1[i], f1 = P.pos1[i + 1];
-    int nrec = 0;  // warp-uniform
-    bool ovf = false;
-    for (int64_t fb = f0; fb < f1; fb += 32) {
-      const int64_t f = fb + lane;
-      int nm = 0;
-      int64_t j = 0, k = 0;
-      double b = 0.0;
-      unsigned long long bc[W], bd[W];
-#pragma unroll
-      for (int w = 0; w < W; w++) bc[w] = bd[w] = 0ull;
-      bool single = false, general = false;
-      int64_t z0 = 0, z1 = 0;
-      if (f < f1) {
-        j = __ldcs(P.idx1 + f);
-        z0 = __ldcs(P.pos2 + f);
-        z1 = __ldcs(P.pos2 + f + 1);
-        load_bm_keep<W>(P.cbm + j * W, keep, bc);
-        if (z1 - z0 == 1) {
-          single = true;
-          k = __ldcs(P.idx2 + z0);
-          b = __ldcs(P.vals + z0);
-          load_bm_keep<W>(P.dbm + k * W, keep, bd);
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            mults += (unsigned long long)__popcll(bd[w]);
-            nm += __popcll(bc[w] & bd[w]);
-          }
-        } else if (z1 > z0) {
-          general = true;
-          // records for the columns of C_j present in some D_k of the fiber
-          unsigned long long any[W];
-#pragma unroll
-          for (int w = 0; w < W; w++) any[w] = 0ull;
-          for (int64_t z = z0; z < z1; z++) {
-            unsigned long long bz[W];
-            load_bm<W>(P.dbm + P.idx2[z] * W, bz);
-#pragma unroll
-            for (int w = 0; w < W; w++) {
-              mults += (unsigned long long)__popcll(bz[w]);
-              any[w] |= bz[w];
-            }
-          }
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            bd[w] = any[w];  // the union, for the match count
-            nm += __popcll(bc[w] & any[w]);
-          }
-        }
-      }
-      const int inc = warp_inclusive_scan(nm);
-      const int tot = __shfl_sync(kFull, inc, 31);
-      if (tot == 0) continue;
-      mults += (unsigned long long)nm;
-      if (ovf || nrec + tot > P.rec_cap) {
-        ovf = true;  // the slice goes to the single-pass kernel
-        continue;
-      }
-      if (nm > 0) {
-        int slot = nrec + inc - nm;
-        const int64_t c0 = ld_val(P.cpos + j, keep);
-        if (single) {
-          const int64_t d0 = ld_val(P.dpos + k, keep);
-          int rc = 0, rd = 0;
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            unsigned long long mm = bc[w] & bd[w];
-            while (mm) {
-              const int bit = __ffsll((long long)mm) - 1;
-              const unsigned long long below = (1ull << bit) - 1ull;
-              rr.ci[slot] = (int32_t)(c0 + rc + __popcll(bc[w] & below));
-              rr.di[slot] = (int32_t)(d0 + rd + __popcll(bd[w] & below));
-              rr.r[slot] = (uint16_t)(w * 64 + bit);
-              rr.b[slot] = b;
-              slot++;
-              mm &= mm - 1ull;
-            }
-            rc += __popcll(bc[w]);
-            rd += __popcll(bd[w]);
-          }
-        } else if (general) {
-          int ic = 0;
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            unsigned long long cm = bc[w];
-            while (cm) {
-              const int bit = __ffsll((long long)cm) - 1;
-              if ((bd[w] >> bit) & 1ull) {
-                const int r = w * 64 + bit;
-                double w0 = 0.0;
-                for (int64_t z = z0; z < z1; z++) {
-                  const int64_t kz = P.idx2[z];
-                  unsigned long long bz[W];
-                  load_bm<W>(P.dbm + kz * W, bz);
-                  if ((bz[w] >> bit) & 1ull)
-                    w0 = add_rn(w0, mul_rn(P.vals[z], P.dvals[P.dpos[kz] + bm_rank<W>(bz, r)]));
-                }
-                rr.ci[slot] = (int32_t)(c0 + ic);
-                rr.di[slot] = -1;  // w0 is final
-                rr.r[slot] = (uint16_t)r;
-                rr.b[slot] = w0;
-                slot++;
-              }
-              ic++;
-              cm &= cm - 1ull;
-            }
-          }
-        }
-      }
-      nrec += tot;
-    }
+#ifndef SPM_D1
+#define SPM_D1 4  // chunks of fiber metadata in flight per warp (power of two)
+#endif
+#ifndef SPM_D2
+#define SPM_D2 2  // chunks of nonzeros in flight per warp (power of two)
+#endif
+#ifndef SPM_GROUP
+#define SPM_GROUP 8  // consecutive slices per claim
+#endif
+#ifndef SPM_CHUNK
+#define SPM_CHUNK 64  // fibers per ring slot
+#endif
+constexpr int kMD1 = SPM_D1, kMD2 = SPM_D2, kMGroup = SPM_GROUP, kMC = SPM_CHUNK;
+constexpr int kMZ = kMC + 8;  // nonzeros staged per chunk
+static_assert(kMD2 < kMD1 && (kMD1 & (kMD1 - 1)) == 0 && (kMD2 & (kMD2 - 1)) == 0, "ring depths");
+static_assert(kMGroup < 32 && kMC % 32 == 0, "groups and chunks");
+
+// A warp's rings.  A chunk is kMC consecutive fibers at an absolute multiple
+// of kMC, so every bulk copy starts on a 16-byte boundary of its array.
+struct __align__(16) MatchRing {
+  int64_t j[kMD1][kMC];
+  int64_t p2[kMD1][kMC + 2];
+  int64_t k[kMD2][kMZ];
+  double v[kMD2][kMZ];
+  int64_t zbase[kMD2];  // first staged nonzero, or -1: lanes read global memory
+  uint64_t bar1[kMD1];
+  uint64_t bar2[kMD2];
+};
+
+// Ring 1: fiber metadata (idx1, pos2) of the chunk starting at fiber f into
+// slot q mod kMD1, one mbarrier phase per use.
+__device__ __forceinline__ void ring_issue1(const SparseParams& P, MatchRing& Q, int lane, uint32_t q,
+                                            int64_t f) {
+  const int s = (int)(q & (kMD1 - 1));
+  if (P.tma_ok && f + kMC + 2 <= P.nfibers + 1) {
     if (lane == 0) {
-      P.rec_cnt[i] = ovf ? -1 : nrec;
-      if (ovf) P.ovf_list[atomicAdd(P.ovf, 1ull)] = i;
+      const uint64_t once = l2_evict_first_policy();
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&Q.bar1[s], 8 * kMC + 8 * (kMC + 2));
+      bulk_g2s_hint(Q.j[s], P.idx1 + f, 8 * kMC, &Q.bar1[s], once);
+      bulk_g2s_hint(Q.p2[s], P.pos2 + f, 8 * (kMC + 2), &Q.bar1[s], once);
+    }
+  } else {
+    // the tensor's last chunk (or arrays off a 16-byte boundary): by the lanes
+    for (int t = lane; t < kMC + 2; t += 32) {
+      if (t < kMC) Q.j[s][t] = f + t < P.nfibers ? P.idx1[f + t] : 0;
+      Q.p2[s][t] = f + t <= P.nfibers ? P.pos2[f + t] : P.nnz;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&Q.bar1[s]);
+  }
+}
+// Ring 2: once the chunk's pos2 range has landed, its nonzeros (idx2, vals)
+// into slot q mod kMD2 (or a note that lanes read them from global memory).
+__device__ __forceinline__ void ring_issue2(const SparseParams& P, MatchRing& Q, int lane, uint32_t q) {
+  const int s1 = (int)(q & (kMD1 - 1)), s2 = (int)(q & (kMD2 - 1));
+  mbar_wait(&Q.bar1[s1], (q / kMD1) & 1u);
+  if (lane == 0) {
+    const int64_t zal = Q.p2[s1][0] & ~(int64_t)1, zbl = (Q.p2[s1][kMC] + 1) & ~(int64_t)1;
+    const int64_t len = zbl - zal;
+    if (P.tma_ok && len > 0 && len <= kMZ && zbl <= P.nnz) {
+      const uint64_t once = l2_evict_first_policy();
+      Q.zbase[s2] = zal;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&Q.bar2[s2], (unsigned)len * 16u);
+      bulk_g2s_hint(Q.k[s2], P.idx2 + zal, (unsigned)len * 8u, &Q.bar2[s2], once);
+      bulk_g2s_hint(Q.v[s2], P.vals + zal, (unsigned)len * 8u, &Q.bar2[s2], once);
+    } else {
+      Q.zbase[s2] = -1;
+      mbar_arrive(&Q.bar2[s2]);
     }
   }
-  mults = warp_sum(mults);
-  if (lane == 0 && mults) atomicAdd(P.mults, mults);
 }
 
-// Phase 2: w0 = 0 + b·D(k,r) in place (a warp per slice, lanes over records).
-__global__ void mttkrp_sparse_dvals_kernel(const SparseParams P) {
+#ifndef SPM_MINB
+#define SPM_MINB 3  // the rings hide the stream's latency: registers before occupancy
+#endif
+template <int W>
+__global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
+    mttkrp_sparse_match_kernel(const __grid_constant__ SparseParams P) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = (int)lane_id();
+  const unsigned lt = lanemask_lt();
+  MatchRing& Q = reinterpret_cast<MatchRing*>(smem_raw)[threadIdx.x >> 5];
+  if (lane == 0) {
+    for (int s = 0; s < kMD1; s++) mbar_init(&Q.bar1[s], 1);
+    for (int s = 0; s < kMD2; s++) mbar_init(&Q.bar2[s], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  uint32_t n1 = 0, n2 = 0, np = 0;  // chunks issued to ring 1 / ring 2 / consumed (warp lifetime)
+  while (true) {
+    int64_t i0 = 0;
+    if (lane == 0) i0 = (int64_t)atomicAdd(P.tile_counter, (unsigned long long)kMGroup);
+    i0 = __shfl_sync(kFull, i0, 0);
+    if (i0 >= P.I) break;
+    const int gcount = (int)min((int64_t)kMGroup, P.I - i0);
+    const int64_t p1 = lane <= gcount ? P.pos1[i0 + lane] : 0;
+    const int64_t F0 = __shfl_sync(kFull, p1, 0);
+    const int64_t fb0 = F0 & ~(int64_t)(kMC - 1);  // first fiber of the group's first chunk
+    // fiber positions below are relative to fb0 (the host bounds a group's fibers to int32)
+    const int p1r = (int)(p1 - fb0);
+    const int F0r = (int)(F0 - fb0), F1r = __shfl_sync(kFull, p1r, gcount);
+    if (F0r == F1r) {
+      if (lane < gcount) P.rec_cnt[i0 + lane] = 0;
+      continue;
+    }
+    const uint32_t nch = (uint32_t)((F1r + kMC - 1) / kMC);
+    const uint32_t base = np;  // n1 == n2 == np between groups
+    for (uint32_t t = 0; t < (uint32_t)kMD1 && t < nch; t++, n1++)
+      ring_issue1(P, Q, lane, n1, fb0 + (int64_t)(n1 - base) * kMC);
+    for (uint32_t t = 0; t < (uint32_t)kMD2 && t < nch; t++, n2++) ring_issue2(P, Q, lane, n2);
+
+    int si = 0;  // current slice of the group
+    int cur_f1 = __shfl_sync(kFull, p1r, 1);
+    int nrec = 0;
+    bool ovf = false;
+    unsigned macc = 0, mcur = 0;  // SPEC multiplications: finished slices / the current one
+    for (uint32_t q = base; q < base + nch; q++) {
+      const int s1 = (int)(q & (kMD1 - 1)), s2 = (int)(q & (kMD2 - 1));
+      mbar_wait(&Q.bar2[s2], (q / kMD2) & 1u);
+      const int64_t zb = Q.zbase[s2];
+#pragma unroll 1
+      for (int h = 0; h < kMC / 32; h++) {
+        const int cfirst = (int)(q - base) * kMC + h * 32;
+        if (cfirst >= F1r) break;
+        const int f = cfirst + lane;
+        const bool valid = f >= F0r && f < F1r;
+        const int t = h * 32 + lane;
+        const int j = (int)Q.j[s1][t];
+        const int64_t z0 = Q.p2[s1][t];
+        const int nz = valid ? (int)(Q.p2[s1][t + 1] - z0) : 0;
+        Bm<W> bc, bd;
+#pragma unroll
+        for (int w = 0; w < W; w++) bc.w[w] = bd.w[w] = 0ull;
+        int nm = 0, k = 0;
+        double b = 0.0;
+        unsigned mf = 0;  // the fiber's SPEC multiplications: |D_k| per nonzero + its w0 entries
+        if (nz >= 1) {
+          const uint64_t keep = l2_evict_last_policy();
+          load_bm_keep<W>(P.cbm + (int64_t)j * W, keep, bc.w);
+          if (zb >= 0) {
+            k = (int)Q.k[s2][z0 - zb];
+            b = Q.v[s2][z0 - zb];
+          } else {
+            k = (int)__ldcs(P.idx2 + z0);
+            b = __ldcs(P.vals + z0);
+          }
+          load_bm_keep<W>(P.dbm + (int64_t)k * W, keep, bd.w);
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            mf += (unsigned)__popcll(bd.w[w]);
+            nm += __popcll(bc.w[w] & bd.w[w]);
+          }
+          mf += (unsigned)nm;
+          if (nz > 1) {
+            // multi-nonzero fiber: one record per (nonzero, column of C_j in its D row);
+            // w0 entries = columns of C_j in the union of the D rows
+            Bm<W> un = bd;
+            for (int64_t z = z0 + 1; z < z0 + nz; z++) {
+              unsigned long long bz[W];
+              load_bm<W>(P.dbm + P.idx2[z] * W, bz);
+#pragma unroll
+              for (int w = 0; w < W; w++) {
+                mf += (unsigned)__popcll(bz[w]);
+                nm += __popcll(bc.w[w] & bz[w]);
+                un.w[w] |= bz[w];
+              }
+            }
+            int groups = 0;
+#pragma unroll
+            for (int w = 0; w < W; w++) groups += __popcll(bc.w[w] & un.w[w]);
+            int first = 0;
+#pragma unroll
+            for (int w = 0; w < W; w++) first += __popcll(bc.w[w] & bd.w[w]);
+            mf += (unsigned)(groups - first);
+          }
+        }
+        const unsigned hits = __ballot_sync(kFull, nm > 0);
+        const bool slow = __any_sync(kFull, nm > 1);  // some lane holds several records
+        // records go to the slice of each lane's fiber: the batch is walked in
+        // segments that end at slice boundaries
+        const int fend = min(cfirst + 32, F1r);
+        int fcur = max(cfirst, F0r);
+        while (si < gcount) {
+          const int seg_end = min(cur_f1, fend);
+          const bool in_seg = f >= fcur && f < seg_end;
+          mcur += in_seg ? mf : 0u;
+          const unsigned hs = hits & __ballot_sync(kFull, in_seg);
+          if (hs) {
+            int before, tot;
+            if (!slow) {
+              before = __popc(hs & lt);
+              tot = __popc(hs);
+            } else {
+              const int x = in_seg ? nm : 0;
+              const int inc = warp_inclusive_scan(x);
+              before = inc - x;
+              tot = __shfl_sync(kFull, inc, 31);
+            }
+            if (ovf || nrec + tot > P.rec_cap) {
+              ovf = true;  // the slice goes to the single-pass kernel
+            } else {
+              if (in_seg && nm > 0) {
+                int slot = nrec + before;
+                const RecRow rr = rec_row(P, i0 + si);
+                if (nz == 1) {
+                  MatchRec rec;
+                  rec.j = j;
+                  rec.k = k;
+                  rec.b = b;
+#pragma unroll
+                  for (int w = 0; w < W; w++) {
+                    unsigned long long mm = bc.w[w] & bd.w[w];
+                    while (mm) {
+                      const int bit = __ffsll((long long)mm) - 1;
+                      rr.rec[slot] = rec;
+                      rr.col[slot] = (uint16_t)((unsigned)(w * 64 + bit) | kRecFirst);
+                      slot++;
+                      mm &= mm - 1ull;
+                    }
+                  }
+                } else {
+                  // column-major, so a column's records are adjacent and in nonzero order
+#pragma unroll
+                  for (int w = 0; w < W; w++) {
+                    unsigned long long cm = bc.w[w];
+                    while (cm) {
+                      const int bit = __ffsll((long long)cm) - 1;
+                      unsigned flag = kRecFirst;
+                      for (int64_t z = z0; z < z0 + nz; z++) {
+                        const int64_t kz = P.idx2[z];
+                        if ((P.dbm[kz * W + w] >> bit) & 1ull) {
+                          MatchRec rec;
+                          rec.j = j;
+                          rec.k = (int)kz;
+                          rec.b = P.vals[z];
+                          rr.rec[slot] = rec;
+                          rr.col[slot] = (uint16_t)((unsigned)(w * 64 + bit) | flag);
+                          slot++;
+                          flag = 0u;
+                        }
+                      }
+                      cm &= cm - 1ull;
+                    }
+                  }
+                }
+              }
+              nrec += tot;
+            }
+          }
+          if (cur_f1 > fend) break;  // the slice continues in a later batch
+          if (lane == 0) {
+            P.rec_cnt[i0 + si] = ovf ? -1 : nrec;
+            if (ovf) P.ovf_list[atomicAdd(P.ovf, 1ull)] = i0 + si;
+          }
+          macc += ovf ? 0u : mcur;  // the single-pass kernel counts its own slices
+          mcur = 0;
+          si++;
+          fcur = cur_f1;
+          cur_f1 = __shfl_sync(kFull, p1r, min(si + 1, 31));
+          nrec = 0;
+          ovf = false;
+        }
+      }
+      __syncwarp();
+      if (n1 < base + nch) {
+        ring_issue1(P, Q, lane, n1, fb0 + (int64_t)(n1 - base) * kMC);
+        n1++;
+      }
+      if (n2 < base + nch) {
+        ring_issue2(P, Q, lane, n2);
+        n2++;
+      }
+    }
+    np = base + nch;
+    const unsigned long long mg = warp_sum((unsigned long long)macc);
+    if (lane == 0 && mg) atomicAdd(P.mults, mg);
+  }
+}
+
+// Phase 2: b·D(k,r) in place (the column's position in D_k from the row's
+// bitmap), and the slice's distinct columns (its row length in A).  A warp
+// per slice, lanes over records.
+template <int W>
+__global__ void __launch_bounds__(256) mttkrp_sparse_dvals_kernel(const SparseParams P) {
+  __shared__ uint32_t pres[8][32];
+  const int lane = (int)lane_id();
+  const int wl = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t keep = l2_evict_last_policy();
   for (int64_t i = warp; i < P.I; i += nwarps) {
     const int n = P.rec_cnt[i];
-    if (n <= 0) continue;
+    if (n <= 0) continue;  // empty (count stays 0) or evaluated by the single-pass kernel
     const RecRow rr = rec_row(P, i);
+    pres[wl][lane] = 0u;
+    __syncwarp();
     for (int t = lane; t < n; t += 32) {
-      const int32_t di = rr.di[t];
-      if (di >= 0) rr.b[t] = add_rn(0.0, mul_rn(rr.b[t], __ldg(P.dvals + di)));
+      const MatchRec rec = rr.rec[t];
+      const int r = (int)(rr.col[t] & 1023u);
+      atomicOr(&pres[wl][r >> 5], 1u << (r & 31));
+      unsigned long long bd[W];
+      load_bm_keep<W>(P.dbm + (int64_t)rec.k * W, keep, bd);
+      const int64_t d = __ldg(P.dpos + rec.k) + bm_rank<W>(bd, r);
+      rr.rec[t].b = mul_rn(rec.b, __ldg(P.dvals + d));
     }
+    __syncwarp();
+    const int cnt = warp_sum(__popc(pres[wl][lane]));
+    if (lane == 0) P.out_pos[i + 1] = cnt;
+    __syncwarp();
   }
 }
 
-// Phase 3: w1(r) += w0·C(j,r) into the warp's workspace, then the sorted
-// drain into the same staging row (its records are consumed by then).
+// Phase 3 (after the row-pointer scan): w0 = 0 + the column's products in
+// order, w1(r) += w0·C(j,r) into the warp's workspace, then the sorted drain
+// straight into the slice's CSR row.  The drain leaves the workspace reset for
+// the next slice.
+template <int W>
 __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(const SparseParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = (int)lane_id();
@@ -1161,22 +1350,32 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(cons
   const size_t ws_bytes = ((size_t)R * 8 + (size_t)nwords * 4 + 15) & ~(size_t)15;
   double* wv = reinterpret_cast<double*>(smem_raw + (size_t)warp * ws_bytes);
   uint32_t* wb = reinterpret_cast<uint32_t*>(wv + R);
+  for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
+  for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
+  __syncwarp();
+  const uint64_t keep = l2_evict_last_policy();
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = gw; i < P.I; i += nwarps) {
     const int n = P.rec_cnt[i];
-    if (n < 0) continue;  // evaluated by the single-pass kernel
-    for (int64_t r = lane; r < R; r += 32) wv[r] = 0.0;
-    for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
-    __syncwarp();
+    if (n <= 0) continue;  // empty, or placed by the overflow compaction
+    const int64_t dst = P.out_pos[i];
     const RecRow rr = rec_row(P, i);
     for (int t = lane; t < n; t += 32) {
-      const double w0 = rr.b[t];
-      ws_add(wv, wb, rr.r[t], mul_rn(w0, __ldg(P.cvals + rr.ci[t])));
+      const unsigned col = rr.col[t];
+      if (!(col & kRecFirst)) continue;  // summed by its column's first record
+      const MatchRec rec = rr.rec[t];
+      const int r = (int)(col & 1023u);
+      double w0 = add_rn(0.0, rec.b);
+      for (int u = t + 1; u < n && !(rr.col[u] & kRecFirst); u++) w0 = add_rn(w0, rr.rec[u].b);
+      unsigned long long bc[W];
+      load_bm_keep<W>(P.cbm + (int64_t)rec.j * W, keep, bc);
+      const int64_t c = __ldg(P.cpos + rec.j) + bm_rank<W>(bc, r);
+      ws_add(wv, wb, (int64_t)r, mul_rn(w0, __ldg(P.cvals + c)));
     }
     __syncwarp();
-    int64_t* oi = P.stage_idx + i * R;
-    double* ov = P.stage_vals + i * R;
+    int64_t* oi = P.out_idx + dst;
+    double* ov = P.out_vals + dst;
     int out = 0;
     for (int w = 0; w < nwords; w++) {
       const uint32_t bits = wb[w];
@@ -1186,11 +1385,32 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(cons
         const int64_t r = (int64_t)w * 32 + lane;
         __stcs(reinterpret_cast<long long*>(oi) + out + rank, (long long)r);
         __stcs(ov + out + rank, wv[r]);
+        wv[r] = 0.0;
       }
       out += __popc(bits);
     }
-    if (lane == 0) P.out_pos[i + 1] = out;
     __syncwarp();
+    for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
+    __syncwarp();
+  }
+}
+
+// Rows of the listed slices (evaluated by the single-pass kernel into their
+// staging rows) into the CSR: a warp per row.
+__global__ void mttkrp_sparse_place_kernel(const SparseParams P) {
+  const int lane = (int)lane_id();
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nlist = (int64_t)*P.nlist_dev;
+  for (int64_t q = warp; q < nlist; q += nwarps) {
+    const int64_t i = P.slice_list[q];
+    const int64_t dst = P.out_pos[i], n = P.out_pos[i + 1] - dst;
+    const int64_t* si = stage_idx_row(P, i);
+    const double* sv = stage_vals_row(P, i);
+    for (int64_t t = lane; t < n; t += 32) {
+      P.out_idx[dst + t] = si[t];
+      P.out_vals[dst + t] = sv[t];
+    }
   }
 }
 
@@ -1201,8 +1421,8 @@ __global__ void mttkrp_sparse_compact_kernel(const SparseParams P) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < P.I; i += nwarps) {
     const int64_t dst = P.out_pos[i], n = P.out_pos[i + 1] - dst;
-    const int64_t* si = P.stage_idx + i * P.R;
-    const double* sv = P.stage_vals + i * P.R;
+    const int64_t* si = stage_idx_row(P, i);
+    const double* sv = stage_vals_row(P, i);
     for (int64_t t = lane; t < n; t += 32) {
       P.out_idx[dst + t] = si[t];
       P.out_vals[dst + t] = sv[t];
@@ -1587,8 +1807,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.dpos = call.device_input(Dv->pos, (size_t)Dv->nrows + 1, Dv->mem);
     P.didx = call.device_input(Dv->idx, (size_t)Dv->nnz, Dv->mem);
     P.dvals = call.device_input(Dv->vals, (size_t)Dv->nnz, Dv->mem);
-    P.stage_idx = call.scratch_n<int64_t>((size_t)(I * R));
-    P.stage_vals = call.scratch_n<double>((size_t)(I * R));
+    P.stage = call.scratch_n<int64_t>((size_t)(2 * I * R));
     auto* ctl = static_cast<uint64_t*>(call.scratch_zero(4 * 8));
     P.tile_counter = reinterpret_cast<unsigned long long*>(ctl);
     P.mults = reinterpret_cast<unsigned long long*>(ctl + 1);
@@ -1652,12 +1871,15 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
         default: launch(mttkrp_sparse_kernel<0>); break;
       }
     };
-    // three phases (match records, D values, C values + drain) when positions
-    // fit int32 and a staging row holds a useful number of records
-    const int rec_cap = (int)((8 * R) / 10) & ~7;
+    // three phases (match records, D values + row counts, C values + drain)
+    // when coordinates fit int32, a staging row holds a useful number of
+    // records (18 bytes each) and most fibers hold one nonzero (a longer
+    // fiber's records are written by one lane)
+    const int rec_cap = (int)((16 * R) / 18) & ~7;
     const char* tp = std::getenv("STAM_SP_PHASES");
-    const bool three = W > 0 && Cv->nnz < INT32_MAX && Dv->nnz < INT32_MAX && R <= 65535 &&
-                       rec_cap >= 32 && !(tp && std::atoi(tp) == 1);
+    const bool three = W > 0 && B->dims[1] < (INT32_MAX - 64) / kMGroup && B->dims[2] < INT32_MAX && R <= 512 &&
+                       rec_cap >= 32 && B->nnz <= B->nfibers + B->nfibers / 8 && !(tp && std::atoi(tp) == 1);
+    const int sms = call.ctx()->num_sms;
     if (!three) {
       launch_single();
     } else {
@@ -1665,13 +1887,18 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       P.rec_cnt = call.scratch_n<int32_t>((size_t)I);
       P.ovf = reinterpret_cast<unsigned long long*>(ctl + 2);
       P.ovf_list = call.scratch_n<int64_t>((size_t)I);
-      const int sms = call.ctx()->num_sms;
+      auto aligned16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
+      P.tma_ok = aligned16(P.idx1) && aligned16(P.pos2) && aligned16(P.idx2) && aligned16(P.vals) &&
+                 std::getenv("STAM_SP_NO_TMA") == nullptr;
       auto match = [&](auto kern) {
+        const size_t msmem = sizeof(MatchRing) * kSpWarps;
+        STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
         int per_sm = 1;
-        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32, 0));
-        const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
+        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32, msmem));
+        const int64_t grid = std::min<int64_t>(ceil_div(ceil_div(I, (int64_t)kMGroup), kSpWarps),
+                                               (int64_t)std::max(1, per_sm) * sms);
         call.before_launch("mttkrp_sparse_match");
-        kern<<<(unsigned)grid, kSpWarps * 32, 0, call.stream()>>>(P);
+        kern<<<(unsigned)grid, kSpWarps * 32, msmem, call.stream()>>>(P);
         call.after_launch();
       };
       switch (W) {
@@ -1680,35 +1907,26 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
         case 4: match(mttkrp_sparse_match_kernel<4>); break;
         default: match(mttkrp_sparse_match_kernel<8>); break;
       }
-      call.before_launch("mttkrp_sparse_dvals");
-      mttkrp_sparse_dvals_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 8), (int64_t)sms * 16), 256, 0,
-                                   call.stream()>>>(P);
-      call.after_launch();
-      {
-        const size_t asmem = ws_bytes * kSpWarps;
-        STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_accum_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-        int per_sm = 1;
-        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mttkrp_sparse_accum_kernel,
-                                                                      kSpWarps * 32, asmem));
-        const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
-        call.before_launch("mttkrp_sparse_accum");
-        mttkrp_sparse_accum_kernel<<<(unsigned)grid, kSpWarps * 32, asmem, call.stream()>>>(P);
-        call.after_launch();
-      }
       // slices with more matches than a staging row holds: the single pass
-      int64_t nov = 0;
-      call.read_scalars(reinterpret_cast<const int64_t*>(ctl + 2), 1, &nov);
-      if (nov > 0) {
-        SparseParams Q = P;
-        Q.slice_list = P.ovf_list;
-        Q.nlist = nov;
-        Q.mults = nullptr;  // counted by the match phase
-        STAM_CUDA_CHECK(cudaMemsetAsync(P.tile_counter, 0, sizeof(unsigned long long), call.stream()));
+      // into their staging rows (the list length stays on the device)
+      {
         const SparseParams saved = P;
-        P = Q;
+        P.slice_list = P.ovf_list;
+        P.nlist_dev = P.ovf;
+        STAM_CUDA_CHECK(cudaMemsetAsync(P.tile_counter, 0, sizeof(unsigned long long), call.stream()));
         launch_single();
         P = saved;
+      }
+      auto dvals = [&](auto kern) {
+        call.before_launch("mttkrp_sparse_dvals");
+        kern<<<(unsigned)std::min<int64_t>(ceil_div(I, 8), (int64_t)sms * 16), 256, 0, call.stream()>>>(P);
+        call.after_launch();
+      };
+      switch (W) {
+        case 1: dvals(mttkrp_sparse_dvals_kernel<1>); break;
+        case 2: dvals(mttkrp_sparse_dvals_kernel<2>); break;
+        case 4: dvals(mttkrp_sparse_dvals_kernel<4>); break;
+        default: dvals(mttkrp_sparse_dvals_kernel<8>); break;
       }
     }
     size_t temp_bytes = 0;
@@ -1727,11 +1945,35 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
                                     cudaMemcpyDeviceToDevice, call.stream()));
     P.out_idx = A->idx;
     P.out_vals = A->vals;
-    call.before_launch("mttkrp_sparse_compact");
-    mttkrp_sparse_compact_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 8),
-                                                               (int64_t)call.ctx()->num_sms * 16),
-                                   256, 0, call.stream()>>>(P);
-    call.after_launch();
+    if (three) {
+      const size_t asmem = ws_bytes * kSpWarps;
+      auto accum = [&](auto kern) {
+        STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+        int per_sm = 1;
+        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32, asmem));
+        const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
+        call.before_launch("mttkrp_sparse_accum");
+        kern<<<(unsigned)grid, kSpWarps * 32, asmem, call.stream()>>>(P);
+        call.after_launch();
+      };
+      switch (W) {
+        case 1: accum(mttkrp_sparse_accum_kernel<1>); break;
+        case 2: accum(mttkrp_sparse_accum_kernel<2>); break;
+        case 4: accum(mttkrp_sparse_accum_kernel<4>); break;
+        default: accum(mttkrp_sparse_accum_kernel<8>); break;
+      }
+      SparseParams Q = P;
+      Q.slice_list = P.ovf_list;
+      Q.nlist_dev = P.ovf;
+      call.before_launch("mttkrp_sparse_place");
+      mttkrp_sparse_place_kernel<<<(unsigned)sms * 2, 256, 0, call.stream()>>>(Q);
+      call.after_launch();
+    } else {
+      call.before_launch("mttkrp_sparse_compact");
+      mttkrp_sparse_compact_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 8), (int64_t)sms * 16), 256, 0,
+                                     call.stream()>>>(P);
+      call.after_launch();
+    }
     call.finish_csr_result(A, nnz);
     call.finish();
     stam_stats* st = call.stats();
