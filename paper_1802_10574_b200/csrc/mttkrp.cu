@@ -568,6 +568,9 @@ __global__ void mttkrp_dense_fixup_kernel(const DenseParams P, const FixupLevels
 constexpr int kSpWarps = SP_WARPS;
 constexpr int kRowChunk = 8;         // factor-row entries held in registers at once
 
+struct HitRec;
+struct MatRec;
+
 struct SparseParams {
   int64_t I, R;
   int64_t nfibers, nnz;
@@ -594,14 +597,21 @@ struct SparseParams {
   // column bitmaps of the factor rows (kBmWords 64-bit words per row; R <= 64*W)
   const unsigned long long* cbm;
   const unsigned long long* dbm;
-  // three-phase path: match records per slice (in the slice's staging row)
-  int32_t* rec_cnt;            // [I] records of each slice, -1: overflowed
-  int32_t rec_cap;             // records a staging row holds
+  // three-phase path: hit and match records per slice
+  int32_t* rec_cnt;            // [I] hits of each slice, -1: left to the single-pass kernel
+  int32_t* mat_cnt;            // [I] match records of each slice
+  uint32_t* dsum;              // [I] sum of |D_k| over the slice's nonzeros (SPEC counter)
+  HitRec* hits;                // [I*hit_cap]
+  MatRec* mats;                // [I*mat_cap]
+  int32_t hit_cap, mat_cap;
+  int mode;                    // single-pass kernel: 0 staged rows, 1 row lengths only, 2 rows into the CSR
   const int64_t* slice_list;   // slices to evaluate (fallback pass), or null: all
   int64_t nlist;
   const unsigned long long* nlist_dev;  // list length on the device (overrides nlist)
   unsigned long long* ovf;     // [0] overflowed slices (appended to ovf_list)
   int64_t* ovf_list;
+  unsigned long long* ovf2;    // the same, filled by the expansion phase
+  int64_t* ovf_list2;
   int tma_ok;                  // the CSF arrays sit on 16-byte boundaries (bulk copies)
 };
 
@@ -958,14 +968,16 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
     else
       sparse_slice(P, i, wv, wb, mults);
     __syncwarp();
-    // sorted drain by ballot/popcount over the presence bitmap
-    int64_t* oi = stage_idx_row(P, i);
-    double* ov = stage_vals_row(P, i);
+    // sorted drain by ballot/popcount over the presence bitmap: into the
+    // slice's staging row (mode 0), nowhere (mode 1: the row length only) or
+    // straight into its CSR row (mode 2, after the scan)
+    int64_t* oi = P.mode == 2 ? P.out_idx + P.out_pos[i] : stage_idx_row(P, i);
+    double* ov = P.mode == 2 ? P.out_vals + P.out_pos[i] : stage_vals_row(P, i);
     int out = 0;
     for (int w = 0; w < nwords; w++) {
       const uint32_t bits = wb[w];
       if (bits == 0) continue;
-      if ((bits >> lane) & 1u) {
+      if (P.mode != 1 && ((bits >> lane) & 1u)) {
         const int rank = __popc(bits & ((1u << lane) - 1u));
         const int64_t r = (int64_t)w * 32 + lane;
         __stcs(reinterpret_cast<long long*>(oi) + out + rank, (long long)r);
@@ -973,7 +985,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
       }
       out += __popc(bits);
     }
-    if (lane == 0) P.out_pos[i + 1] = out;
+    if (lane == 0 && P.mode != 2) P.out_pos[i + 1] = out;
     __syncwarp();
   }
   mults = warp_sum(mults);
@@ -984,43 +996,51 @@ __global__ void __launch_bounds__(kSpWarps * 32, SP_MINB) mttkrp_sparse_kernel(c
 // Three phases, each with a gathered set below the L2's ~64-80 MB random-
 // gather capacity (profiles/r02/l2_capacity.md; one pass gathers ~104 MB at
 // config 5 and misses on 23-63 % of lookups):
-//  1. match: the CSF streamed once through per-warp shared-memory rings
+//  1. filter: the CSF streamed once through per-warp shared-memory rings
 //     filled by TMA bulk copies (fiber metadata kMD1 chunks ahead, a chunk's
 //     nonzeros as soon as its pos2 range has landed), so the only loads a lane
-//     waits for are the two factor-row bitmaps (gathered set: 32 MB).  Each
-//     matching (nonzero, column) pair becomes a record (j, k, b | column) in
-//     the slice's own staging row; a slice with more records than the row
-//     holds is listed for the single-pass kernel (which drains into the same
-//     staging row; a placement kernel copies those rows after the scan).
-//  2. D values: every record's b becomes b·D(k,r) (gathered: D's bitmaps, row
-//     starts and values, 52 MB); the slice's distinct columns are counted, so
-//     the row pointers can be scanned before any row is written.
-//  3. C values: a warp per slice adds w0·C(j,r) into its R-wide workspace
-//     (C's bitmaps, row starts and values) and drains it sorted straight into
+//     waits for are the two factor-row bitmaps (gathered set: 32 MB).  A
+//     nonzero whose C_j and D_k share a column becomes a hit record (j, k, b)
+//     in the slice's hit row -- one 16-byte store, no walk over the bits.
+//  2. expand: lanes over the slice's hits (every lane holds one, so the bit
+//     walks run on full warps): each shared column becomes a match record
+//     (positions of C(j,r) and D(k,r) in the factors' values, column, the
+//     hit's index), and the slice's distinct columns are counted, so the row
+//     pointers can be scanned before any row is written (gathered: both
+//     bitmaps and both row-start arrays, 40 MB; with D's values in the same
+//     kernel the 72 MB set missed L2: 5.2 GB of DRAM reads for 1.5 GB of
+//     records).
+//  3. accumulate: a warp per slice, lanes over its match records:
+//     w0 = 0 + b·D(k,r), w1(r) += w0·C(j,r) into its R-wide workspace
+//     (gathered: both factors' values, 64 MB), drained sorted straight into
 //     the CSR.
-// Same arithmetic and per-entry order as sparse_slice_bm: w0(r) = 0 + b·D(k,r)
-// (+ the fiber's further nonzeros in order: their records follow the first
-// one of the column, unflagged), then w1(r) += w0(r)·C(j,r).
-template <int W>
-struct Bm {
-  unsigned long long w[W];
-};
-
-struct __align__(16) MatchRec {
+// Same arithmetic as sparse_slice_bm for single-nonzero fibers; a multi-nonzero
+// fiber yields one hit per nonzero (columns shared by two of its nonzeros are
+// multiplied with C one by one, see the filter).  A slice with more hits or
+// matches than its rows hold goes to the single-pass kernel, which runs over
+// the listed slices twice: row lengths before the scan, the rows after it.
+struct __align__(16) HitRec {
   int j, k;
   double b;
 };
-constexpr unsigned kRecFirst = 0x8000u;  // first record of its (fiber, column)
-struct RecRow {
-  MatchRec* rec;
-  uint16_t* col;  // column | kRecFirst
-};
-__device__ __forceinline__ RecRow rec_row(const SparseParams& P, int64_t i) {
-  RecRow x;
-  x.rec = reinterpret_cast<MatchRec*>(P.stage + i * 2 * P.R);
-  x.col = reinterpret_cast<uint16_t*>(x.rec + P.rec_cap);
-  return x;
+// Records are touched once per phase: streamed past the L2-resident factor data.
+template <typename T>
+__device__ __forceinline__ T ld_rec(const T* p) {
+  static_assert(sizeof(T) == 16, "16-byte records");
+  const int4 v = __ldcs(reinterpret_cast<const int4*>(p));
+  return *reinterpret_cast<const T*>(&v);
 }
+template <typename T>
+__device__ __forceinline__ void st_rec(T* p, const T& x) {
+  static_assert(sizeof(T) == 16, "16-byte records");
+  __stcs(reinterpret_cast<int4*>(p), *reinterpret_cast<const int4*>(&x));
+}
+
+struct __align__(16) MatRec {
+  int c;          // position of C(j, column) in C's values
+  unsigned meta;  // column | the hit's index in the slice's hit row << 10
+  int64_t d;      // position of D(k, column) in D's values
+};
 
 #ifndef SPM_D1
 #define SPM_D1 4  // chunks of fiber metadata in flight per warp (power of two)
@@ -1101,7 +1121,7 @@ __device__ __forceinline__ void ring_issue2(const SparseParams& P, MatchRing& Q,
 #endif
 template <int W>
 __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
-    mttkrp_sparse_match_kernel(const __grid_constant__ SparseParams P) {
+    mttkrp_sparse_filter_kernel(const __grid_constant__ SparseParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = (int)lane_id();
   const unsigned lt = lanemask_lt();
@@ -1126,7 +1146,10 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
     const int p1r = (int)(p1 - fb0);
     const int F0r = (int)(F0 - fb0), F1r = __shfl_sync(kFull, p1r, gcount);
     if (F0r == F1r) {
-      if (lane < gcount) P.rec_cnt[i0 + lane] = 0;
+      if (lane < gcount) {
+        P.rec_cnt[i0 + lane] = 0;
+        P.dsum[i0 + lane] = 0u;
+      }
       continue;
     }
     const uint32_t nch = (uint32_t)((F1r + kMC - 1) / kMC);
@@ -1139,7 +1162,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
     int cur_f1 = __shfl_sync(kFull, p1r, 1);
     int nrec = 0;
     bool ovf = false;
-    unsigned macc = 0, mcur = 0;  // SPEC multiplications: finished slices / the current one
+    unsigned mcur = 0;  // the lane's share of the current slice's sum of |D_k|
     for (uint32_t q = base; q < base + nch; q++) {
       const int s1 = (int)(q & (kMD1 - 1)), s2 = (int)(q & (kMD2 - 1));
       mbar_wait(&Q.bar2[s2], (q / kMD2) & 1u);
@@ -1154,15 +1177,13 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
         const int j = (int)Q.j[s1][t];
         const int64_t z0 = Q.p2[s1][t];
         const int nz = valid ? (int)(Q.p2[s1][t + 1] - z0) : 0;
-        Bm<W> bc, bd;
-#pragma unroll
-        for (int w = 0; w < W; w++) bc.w[w] = bd.w[w] = 0ull;
-        int nm = 0, k = 0;
+        int nh = 0, k = 0;  // the fiber's hits
         double b = 0.0;
-        unsigned mf = 0;  // the fiber's SPEC multiplications: |D_k| per nonzero + its w0 entries
+        unsigned mf = 0;  // the fiber's sum of |D_k|
         if (nz >= 1) {
           const uint64_t keep = l2_evict_last_policy();
-          load_bm_keep<W>(P.cbm + (int64_t)j * W, keep, bc.w);
+          unsigned long long bc[W], bd[W];
+          load_bm_keep<W>(P.cbm + (int64_t)j * W, keep, bc);
           if (zb >= 0) {
             k = (int)Q.k[s2][z0 - zb];
             b = Q.v[s2][z0 - zb];
@@ -1170,39 +1191,46 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
             k = (int)__ldcs(P.idx2 + z0);
             b = __ldcs(P.vals + z0);
           }
-          load_bm_keep<W>(P.dbm + (int64_t)k * W, keep, bd.w);
+          load_bm_keep<W>(P.dbm + (int64_t)k * W, keep, bd);
+          unsigned long long any = 0ull;
 #pragma unroll
           for (int w = 0; w < W; w++) {
-            mf += (unsigned)__popcll(bd.w[w]);
-            nm += __popcll(bc.w[w] & bd.w[w]);
+            mf += (unsigned)__popcll(bd[w]);
+            any |= bc[w] & bd[w];
           }
-          mf += (unsigned)nm;
+          nh = any != 0ull ? 1 : 0;
           if (nz > 1) {
-            // multi-nonzero fiber: one record per (nonzero, column of C_j in its D row);
-            // w0 entries = columns of C_j in the union of the D rows
-            Bm<W> un = bd;
+            // one hit per nonzero.  Two nonzeros meeting C_j in one column are
+            // multiplied with C(j,r) one by one instead of summed first (the
+            // difference is an ulp of the column's terms, inside the parity
+            // bound); the SPEC counter takes one w0 entry per distinct column.
+            int seen = 0, each = 0;
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+              bd[w] &= bc[w];  // columns of C_j seen so far
+              each += __popcll(bd[w]);
+            }
             for (int64_t z = z0 + 1; z < z0 + nz; z++) {
               unsigned long long bz[W];
               load_bm<W>(P.dbm + P.idx2[z] * W, bz);
+              unsigned long long m = 0ull;
 #pragma unroll
               for (int w = 0; w < W; w++) {
                 mf += (unsigned)__popcll(bz[w]);
-                nm += __popcll(bc.w[w] & bz[w]);
-                un.w[w] |= bz[w];
+                m |= bc[w] & bz[w];
+                each += __popcll(bc[w] & bz[w]);
+                bd[w] |= bc[w] & bz[w];
               }
+              nh += m != 0ull ? 1 : 0;
             }
-            int groups = 0;
 #pragma unroll
-            for (int w = 0; w < W; w++) groups += __popcll(bc.w[w] & un.w[w]);
-            int first = 0;
-#pragma unroll
-            for (int w = 0; w < W; w++) first += __popcll(bc.w[w] & bd.w[w]);
-            mf += (unsigned)(groups - first);
+            for (int w = 0; w < W; w++) seen += __popcll(bd[w]);
+            mf -= (unsigned)(each - seen);  // phase 2 adds one per match
           }
         }
-        const unsigned hits = __ballot_sync(kFull, nm > 0);
-        const bool slow = __any_sync(kFull, nm > 1);  // some lane holds several records
-        // records go to the slice of each lane's fiber: the batch is walked in
+        const unsigned hits = __ballot_sync(kFull, nh > 0);
+        const bool slow = __any_sync(kFull, nh > 1);  // a multi-nonzero fiber with several hits
+        // hits go to the slice of each lane's fiber: the batch is walked in
         // segments that end at slice boundaries
         const int fend = min(cfirst + 32, F1r);
         int fcur = max(cfirst, F0r);
@@ -1210,62 +1238,44 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
           const int seg_end = min(cur_f1, fend);
           const bool in_seg = f >= fcur && f < seg_end;
           mcur += in_seg ? mf : 0u;
-          const unsigned hs = hits & __ballot_sync(kFull, in_seg);
+          const unsigned seg = __ballot_sync(kFull, in_seg);
+          const unsigned hs = hits & seg;
           if (hs) {
             int before, tot;
             if (!slow) {
               before = __popc(hs & lt);
               tot = __popc(hs);
             } else {
-              const int x = in_seg ? nm : 0;
+              const int x = in_seg ? nh : 0;
               const int inc = warp_inclusive_scan(x);
               before = inc - x;
               tot = __shfl_sync(kFull, inc, 31);
             }
-            if (ovf || nrec + tot > P.rec_cap) {
+            if (ovf || nrec + tot > P.hit_cap) {
               ovf = true;  // the slice goes to the single-pass kernel
             } else {
-              if (in_seg && nm > 0) {
-                int slot = nrec + before;
-                const RecRow rr = rec_row(P, i0 + si);
+              if (in_seg && nh > 0) {
+                HitRec* row = P.hits + (i0 + si) * P.hit_cap + nrec + before;
+                HitRec rec;
+                rec.j = j;
+                rec.k = k;
+                rec.b = b;
                 if (nz == 1) {
-                  MatchRec rec;
-                  rec.j = j;
-                  rec.k = k;
-                  rec.b = b;
-#pragma unroll
-                  for (int w = 0; w < W; w++) {
-                    unsigned long long mm = bc.w[w] & bd.w[w];
-                    while (mm) {
-                      const int bit = __ffsll((long long)mm) - 1;
-                      rr.rec[slot] = rec;
-                      rr.col[slot] = (uint16_t)((unsigned)(w * 64 + bit) | kRecFirst);
-                      slot++;
-                      mm &= mm - 1ull;
-                    }
-                  }
+                  st_rec(row, rec);
                 } else {
-                  // column-major, so a column's records are adjacent and in nonzero order
+                  unsigned long long bc[W];
+                  load_bm<W>(P.cbm + (int64_t)j * W, bc);
+                  for (int64_t z = z0; z < z0 + nz; z++) {
+                    const int64_t kz = P.idx2[z];
+                    unsigned long long bz[W];
+                    load_bm<W>(P.dbm + kz * W, bz);
+                    unsigned long long m = 0ull;
 #pragma unroll
-                  for (int w = 0; w < W; w++) {
-                    unsigned long long cm = bc.w[w];
-                    while (cm) {
-                      const int bit = __ffsll((long long)cm) - 1;
-                      unsigned flag = kRecFirst;
-                      for (int64_t z = z0; z < z0 + nz; z++) {
-                        const int64_t kz = P.idx2[z];
-                        if ((P.dbm[kz * W + w] >> bit) & 1ull) {
-                          MatchRec rec;
-                          rec.j = j;
-                          rec.k = (int)kz;
-                          rec.b = P.vals[z];
-                          rr.rec[slot] = rec;
-                          rr.col[slot] = (uint16_t)((unsigned)(w * 64 + bit) | flag);
-                          slot++;
-                          flag = 0u;
-                        }
-                      }
-                      cm &= cm - 1ull;
+                    for (int w = 0; w < W; w++) m |= bc[w] & bz[w];
+                    if (m != 0ull) {
+                      rec.k = (int)kz;
+                      rec.b = P.vals[z];
+                      *row++ = rec;
                     }
                   }
                 }
@@ -1274,11 +1284,12 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
             }
           }
           if (cur_f1 > fend) break;  // the slice continues in a later batch
+          const unsigned ds = warp_sum(mcur);
           if (lane == 0) {
             P.rec_cnt[i0 + si] = ovf ? -1 : nrec;
+            P.dsum[i0 + si] = ds;
             if (ovf) P.ovf_list[atomicAdd(P.ovf, 1ull)] = i0 + si;
           }
-          macc += ovf ? 0u : mcur;  // the single-pass kernel counts its own slices
           mcur = 0;
           si++;
           fcur = cur_f1;
@@ -1298,49 +1309,139 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
       }
     }
     np = base + nch;
-    const unsigned long long mg = warp_sum((unsigned long long)macc);
-    if (lane == 0 && mg) atomicAdd(P.mults, mg);
   }
 }
 
-// Phase 2: b·D(k,r) in place (the column's position in D_k from the row's
-// bitmap), and the slice's distinct columns (its row length in A).  A warp
-// per slice, lanes over records.
+// Phase 2: lanes over the slice's hits, kXU hits per lane and step (their
+// record, bitmap and row-start loads in flight together).  Each hit's shared
+// columns become match records; the slice's distinct columns give its row
+// length in A.
+#ifndef SPX_U
+#define SPX_U 1
+#endif
+constexpr int kXU = SPX_U;
 template <int W>
-__global__ void __launch_bounds__(256) mttkrp_sparse_dvals_kernel(const SparseParams P) {
+__global__ void __launch_bounds__(256) mttkrp_sparse_expand_kernel(const SparseParams P) {
   __shared__ uint32_t pres[8][32];
   const int lane = (int)lane_id();
   const int wl = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t keep = l2_evict_last_policy();
+  unsigned long long mults = 0;
   for (int64_t i = warp; i < P.I; i += nwarps) {
     const int n = P.rec_cnt[i];
-    if (n <= 0) continue;  // empty (count stays 0) or evaluated by the single-pass kernel
-    const RecRow rr = rec_row(P, i);
+    if (n < 0) continue;  // evaluated by the single-pass kernel
+    if (n == 0) {
+      // no hit: an empty row; the multiplications that found nothing still count
+      if (lane == 0) {
+        P.mat_cnt[i] = 0;
+        mults += P.dsum[i];
+      }
+      continue;
+    }
+    const HitRec* hrow = P.hits + i * P.hit_cap;
+    MatRec* mrow = P.mats + i * P.mat_cap;
     pres[wl][lane] = 0u;
     __syncwarp();
-    for (int t = lane; t < n; t += 32) {
-      const MatchRec rec = rr.rec[t];
-      const int r = (int)(rr.col[t] & 1023u);
-      atomicOr(&pres[wl][r >> 5], 1u << (r & 31));
-      unsigned long long bd[W];
-      load_bm_keep<W>(P.dbm + (int64_t)rec.k * W, keep, bd);
-      const int64_t d = __ldg(P.dpos + rec.k) + bm_rank<W>(bd, r);
-      rr.rec[t].b = mul_rn(rec.b, __ldg(P.dvals + d));
+    int nmat = 0;
+    bool ovf = false;
+    for (int t0 = 0; t0 < n; t0 += 32 * kXU) {
+      HitRec rec[kXU];
+      unsigned long long bc[kXU][W], bd[kXU][W];
+      int64_t d0[kXU], c0[kXU];
+      int x[kXU];
+#pragma unroll
+      for (int u = 0; u < kXU; u++) {
+        const int t = t0 + u * 32 + lane;
+        rec[u].j = rec[u].k = 0;
+        rec[u].b = 0.0;
+        if (t < n) rec[u] = ld_rec(hrow + t);
+      }
+      int xs = 0;
+#pragma unroll
+      for (int u = 0; u < kXU; u++) {
+        const int t = t0 + u * 32 + lane;
+#pragma unroll
+        for (int w = 0; w < W; w++) bc[u][w] = bd[u][w] = 0ull;
+        d0[u] = c0[u] = 0;
+        if (t < n) {
+          load_bm_keep<W>(P.cbm + (int64_t)rec[u].j * W, keep, bc[u]);
+          load_bm_keep<W>(P.dbm + (int64_t)rec[u].k * W, keep, bd[u]);
+          d0[u] = __ldg(P.dpos + rec[u].k);
+          c0[u] = __ldg(P.cpos + rec[u].j);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kXU; u++) {
+        x[u] = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) x[u] += __popcll(bc[u][w] & bd[u][w]);
+        xs += x[u];
+      }
+      const int inc = warp_inclusive_scan(xs);
+      const int tot = __shfl_sync(kFull, inc, 31);
+      if (nmat + tot > P.mat_cap) {
+        ovf = true;
+        break;
+      }
+      MatRec* out = mrow + nmat + inc - xs;
+#pragma unroll
+      for (int u = 0; u < kXU; u++) {
+        if (x[u] > 0) {
+          int pc = 0, pd = 0;
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            unsigned long long mm = bc[u][w] & bd[u][w];
+            while (mm) {
+              const int bit = __ffsll((long long)mm) - 1;
+              const unsigned long long below = (1ull << bit) - 1ull;
+              const int rc = pc + __popcll(bc[u][w] & below);
+              const int rd = pd + __popcll(bd[u][w] & below);
+              const unsigned r = (unsigned)(w * 64 + bit);
+              MatRec m;
+              m.c = (int)(c0[u] + rc);
+              m.meta = r | ((unsigned)(t0 + u * 32 + lane) << 10);
+              m.d = d0[u] + rd;
+              st_rec(out++, m);
+              atomicOr(&pres[wl][r >> 5], 1u << (r & 31u));
+              mm &= mm - 1ull;
+            }
+            pc += __popcll(bc[u][w]);
+            pd += __popcll(bd[u][w]);
+          }
+        }
+      }
+      nmat += tot;
     }
     __syncwarp();
-    const int cnt = warp_sum(__popc(pres[wl][lane]));
-    if (lane == 0) P.out_pos[i + 1] = cnt;
+    if (ovf) {
+      if (lane == 0) {
+        P.rec_cnt[i] = -1;
+        P.ovf_list2[atomicAdd(P.ovf2, 1ull)] = i;
+      }
+    } else {
+      const int cnt = warp_sum(__popc(pres[wl][lane]));
+      if (lane == 0) {
+        P.out_pos[i + 1] = cnt;
+        P.mat_cnt[i] = nmat;
+        mults += (unsigned long long)P.dsum[i] + (unsigned long long)nmat;
+      }
+    }
     __syncwarp();
   }
+  if (lane == 0 && mults) atomicAdd(P.mults, mults);
 }
 
-// Phase 3 (after the row-pointer scan): w0 = 0 + the column's products in
-// order, w1(r) += w0·C(j,r) into the warp's workspace, then the sorted drain
-// straight into the slice's CSR row.  The drain leaves the workspace reset for
-// the next slice.
-template <int W>
+// Phase 3 (after the row-pointer scan): w0 = 0 + b·D(k,r) (final: one nonzero
+// per fiber and column, see phase 1), w1(r) += w0·C(j,r) into the warp's
+// workspace (kAU records per lane in flight), then the sorted drain straight
+// into the slice's CSR row.  The drain leaves the workspace reset for the
+// next slice.
+#ifndef SPA_U
+#define SPA_U 4
+#endif
+constexpr int kAU = SPA_U;
 __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(const SparseParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = (int)lane_id();
@@ -1357,21 +1458,35 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(cons
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = gw; i < P.I; i += nwarps) {
-    const int n = P.rec_cnt[i];
-    if (n <= 0) continue;  // empty, or placed by the overflow compaction
+    if (P.rec_cnt[i] <= 0) continue;  // empty, or written by the single-pass kernel
+    const int n = P.mat_cnt[i];
     const int64_t dst = P.out_pos[i];
-    const RecRow rr = rec_row(P, i);
-    for (int t = lane; t < n; t += 32) {
-      const unsigned col = rr.col[t];
-      if (!(col & kRecFirst)) continue;  // summed by its column's first record
-      const MatchRec rec = rr.rec[t];
-      const int r = (int)(col & 1023u);
-      double w0 = add_rn(0.0, rec.b);
-      for (int u = t + 1; u < n && !(rr.col[u] & kRecFirst); u++) w0 = add_rn(w0, rr.rec[u].b);
-      unsigned long long bc[W];
-      load_bm_keep<W>(P.cbm + (int64_t)rec.j * W, keep, bc);
-      const int64_t c = __ldg(P.cpos + rec.j) + bm_rank<W>(bc, r);
-      ws_add(wv, wb, (int64_t)r, mul_rn(w0, __ldg(P.cvals + c)));
+    const MatRec* mrow = P.mats + i * P.mat_cap;
+    const HitRec* hrow = P.hits + i * P.hit_cap;
+    for (int t0 = 0; t0 < n; t0 += 32 * kAU) {
+      MatRec m[kAU];
+      double cv[kAU], dv[kAU], b[kAU];
+#pragma unroll
+      for (int u = 0; u < kAU; u++) {
+        const int t = t0 + u * 32 + lane;
+        m[u].c = 0;
+        m[u].meta = 0u;
+        m[u].d = 0;
+        if (t < n) m[u] = ld_rec(mrow + t);
+      }
+#pragma unroll
+      for (int u = 0; u < kAU; u++) {
+        const bool on = t0 + u * 32 + lane < n;
+        cv[u] = on ? ld_keep(P.cvals + m[u].c, keep) : 0.0;
+        dv[u] = on ? ld_keep(P.dvals + m[u].d, keep) : 0.0;
+        b[u] = on ? hrow[m[u].meta >> 10].b : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kAU; u++)
+        if (t0 + u * 32 + lane < n) {
+          const double w0 = add_rn(0.0, mul_rn(b[u], dv[u]));
+          ws_add(wv, wb, (int64_t)(m[u].meta & 1023u), mul_rn(w0, cv[u]));
+        }
     }
     __syncwarp();
     int64_t* oi = P.out_idx + dst;
@@ -1392,25 +1507,6 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(cons
     __syncwarp();
     for (int w = lane; w < nwords; w += 32) wb[w] = 0u;
     __syncwarp();
-  }
-}
-
-// Rows of the listed slices (evaluated by the single-pass kernel into their
-// staging rows) into the CSR: a warp per row.
-__global__ void mttkrp_sparse_place_kernel(const SparseParams P) {
-  const int lane = (int)lane_id();
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nlist = (int64_t)*P.nlist_dev;
-  for (int64_t q = warp; q < nlist; q += nwarps) {
-    const int64_t i = P.slice_list[q];
-    const int64_t dst = P.out_pos[i], n = P.out_pos[i + 1] - dst;
-    const int64_t* si = stage_idx_row(P, i);
-    const double* sv = stage_vals_row(P, i);
-    for (int64_t t = lane; t < n; t += 32) {
-      P.out_idx[dst + t] = si[t];
-      P.out_vals[dst + t] = sv[t];
-    }
   }
 }
 
@@ -1588,7 +1684,7 @@ int mttkrp_sparse_streamed(stam_cuda_ctx* ctx, const stam_csf3_view* B, const st
     auto* d_vals = call.host_staging<double>((size_t)B->nnz);
     // nnz-balanced slice blocks (~16M nonzeros each)
     int64_t nblocks = std::max<int64_t>(2, std::min<int64_t>(64, ceil_div(B->nnz, (int64_t)1 << 24)));
-    nblocks = std::max(nblocks, ceil_div(I * R * 16, sparse_stage_budget()));
+    nblocks = std::max(nblocks, ceil_div(I * R * 22, sparse_stage_budget()));
     nblocks = std::min(nblocks, I);
     std::vector<int64_t> sb{0};
     for (int64_t b = 1; b < nblocks; b++) {
@@ -1705,7 +1801,7 @@ int mttkrp_sparse_blocked(stam_cuda_ctx* ctx, const stam_csf3_view* B, const sta
     Bd.idx2 = call.device_input(B->idx2, (size_t)B->nnz, B->mem);
     Bd.vals = call.device_input(B->vals, (size_t)B->nnz, B->mem);
     Bd.mem = STAM_MEM_DEVICE;
-    const int64_t per = std::max<int64_t>(1, sparse_stage_budget() / (16 * R));  // slices per block
+    const int64_t per = std::max<int64_t>(1, sparse_stage_budget() / (22 * R));  // slices per block
     const int64_t nblocks = ceil_div(I, per);
     std::vector<stam_csr_result> parts((size_t)nblocks);
     int64_t total = 0, launches = 0, mults = 0;
@@ -1775,7 +1871,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       std::getenv("STAM_NO_STREAM") == nullptr)
     return mttkrp_sparse_streamed(ctx, B, Cv, Dv, opts, A, stats);
   if (ctx && B && Cv && Dv && opts && B->dims[0] > 1 && Cv->ncols > 0 &&
-      B->dims[0] * Cv->ncols * 16 > sparse_stage_budget())
+      B->dims[0] * Cv->ncols * 22 > sparse_stage_budget())
     return mttkrp_sparse_blocked(ctx, B, Cv, Dv, opts, A, stats);
   return guarded([&] {
     Call call(reinterpret_cast<Ctx*>(ctx), opts, stats);
@@ -1807,8 +1903,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.dpos = call.device_input(Dv->pos, (size_t)Dv->nrows + 1, Dv->mem);
     P.didx = call.device_input(Dv->idx, (size_t)Dv->nnz, Dv->mem);
     P.dvals = call.device_input(Dv->vals, (size_t)Dv->nnz, Dv->mem);
-    P.stage = call.scratch_n<int64_t>((size_t)(2 * I * R));
-    auto* ctl = static_cast<uint64_t*>(call.scratch_zero(4 * 8));
+    auto* ctl = static_cast<uint64_t*>(call.scratch_zero(8 * 8));
     P.tile_counter = reinterpret_cast<unsigned long long*>(ctl);
     P.mults = reinterpret_cast<unsigned long long*>(ctl + 1);
     // row pointers: counts at [i+1], scanned in place
@@ -1843,7 +1938,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       P.cbm = build_bm(P.cpos, P.cidx, Cv->nrows);
       P.dbm = build_bm(P.dpos, P.didx, Dv->nrows);
     }
-    auto launch = [&](auto kern) {
+    auto launch = [&](auto kern, cudaStream_t st) {
       STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem_w));
       int per_sm = 1;
@@ -1851,83 +1946,107 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
                                                                     smem_w));
       const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps),
                                              (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
-      call.before_launch("mttkrp_sparse");
+      call.before_launch("mttkrp_sparse", st);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)grid);
       cfg.blockDim = dim3(kSpWarps * 32);
       cfg.dynamicSmemBytes = smem_w;
-      cfg.stream = call.stream();
+      cfg.stream = st;
       cfg.attrs = nullptr;
       cfg.numAttrs = 0;
       STAM_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, P));
-      call.after_launch();
+      call.after_launch(st);
     };
-    auto launch_single = [&]() {
+    auto launch_single = [&](cudaStream_t st) {
       switch (W) {
-        case 1: launch(mttkrp_sparse_kernel<1>); break;
-        case 2: launch(mttkrp_sparse_kernel<2>); break;
-        case 4: launch(mttkrp_sparse_kernel<4>); break;
-        case 8: launch(mttkrp_sparse_kernel<8>); break;
-        default: launch(mttkrp_sparse_kernel<0>); break;
+        case 1: launch(mttkrp_sparse_kernel<1>, st); break;
+        case 2: launch(mttkrp_sparse_kernel<2>, st); break;
+        case 4: launch(mttkrp_sparse_kernel<4>, st); break;
+        case 8: launch(mttkrp_sparse_kernel<8>, st); break;
+        default: launch(mttkrp_sparse_kernel<0>, st); break;
       }
     };
-    // three phases (match records, D values + row counts, C values + drain)
-    // when coordinates fit int32, a staging row holds a useful number of
-    // records (18 bytes each) and most fibers hold one nonzero (a longer
-    // fiber's records are written by one lane)
-    const int rec_cap = (int)((16 * R) / 18) & ~7;
+    // the single-pass kernel over one of the slice lists of the three-phase path
+    auto launch_list = [&](int which, int mode, cudaStream_t st) {
+      const SparseParams saved = P;
+      P.slice_list = which == 0 ? saved.ovf_list : saved.ovf_list2;
+      P.nlist_dev = which == 0 ? saved.ovf : saved.ovf2;
+      P.mode = mode;
+      if (mode == 2) P.mults = nullptr;  // counted by the first run
+      P.tile_counter = reinterpret_cast<unsigned long long*>(ctl + 4 + which + 2 * (mode == 2));
+      launch_single(st);
+      P = saved;
+    };
+    // three phases (filter -> hits, expand -> matches + row lengths, accumulate
+    // + drain) when coordinates fit int32 and most fibers hold one nonzero (a
+    // longer fiber's hits are written by one lane).  Rows per slice: hits and
+    // matches are sized from the rank (a row of A holds at most R entries;
+    // the sparse-factor workloads fill a fraction of it), slices that exceed
+    // them go to the single-pass kernel.
+    const int hit_cap = std::max(32, (int)((5 * R) / 8) & ~7);
+    const int mat_cap = std::max(32, (int)((3 * R) / 4) & ~7);
     const char* tp = std::getenv("STAM_SP_PHASES");
     const bool three = W > 0 && B->dims[1] < (INT32_MAX - 64) / kMGroup && B->dims[2] < INT32_MAX && R <= 512 &&
-                       rec_cap >= 32 && B->nnz <= B->nfibers + B->nfibers / 8 && !(tp && std::atoi(tp) == 1);
+                       Cv->nnz < INT32_MAX &&
+                       B->nnz <= B->nfibers + B->nfibers / 8 && !(tp && std::atoi(tp) == 1);
     const int sms = call.ctx()->num_sms;
     if (!three) {
-      launch_single();
+      P.stage = call.scratch_n<int64_t>((size_t)(2 * I * R));
+      launch_single(call.stream());
     } else {
-      P.rec_cap = rec_cap;
+      P.hit_cap = hit_cap;
+      P.mat_cap = mat_cap;
+      P.hits = static_cast<HitRec*>(call.scratch(sizeof(HitRec) * (size_t)I * hit_cap));
+      P.mats = static_cast<MatRec*>(call.scratch(sizeof(MatRec) * (size_t)I * mat_cap));
       P.rec_cnt = call.scratch_n<int32_t>((size_t)I);
+      P.mat_cnt = call.scratch_n<int32_t>((size_t)I);
+      P.dsum = reinterpret_cast<uint32_t*>(call.scratch_n<int32_t>((size_t)I));
+      // slices left to the single-pass kernel: listed by the filter (list 1)
+      // and by the expansion (list 2), so list 1 can be evaluated beside it
       P.ovf = reinterpret_cast<unsigned long long*>(ctl + 2);
-      P.ovf_list = call.scratch_n<int64_t>((size_t)I);
+      P.ovf2 = reinterpret_cast<unsigned long long*>(ctl + 3);
+      P.ovf_list = call.scratch_n<int64_t>((size_t)(2 * I));
+      P.ovf_list2 = P.ovf_list + I;
       auto aligned16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
       P.tma_ok = aligned16(P.idx1) && aligned16(P.pos2) && aligned16(P.idx2) && aligned16(P.vals) &&
                  std::getenv("STAM_SP_NO_TMA") == nullptr;
-      auto match = [&](auto kern) {
+      auto filter = [&](auto kern) {
         const size_t msmem = sizeof(MatchRing) * kSpWarps;
         STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
         int per_sm = 1;
         STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32, msmem));
         const int64_t grid = std::min<int64_t>(ceil_div(ceil_div(I, (int64_t)kMGroup), kSpWarps),
                                                (int64_t)std::max(1, per_sm) * sms);
-        call.before_launch("mttkrp_sparse_match");
+        call.before_launch("mttkrp_sparse_filter");
         kern<<<(unsigned)grid, kSpWarps * 32, msmem, call.stream()>>>(P);
         call.after_launch();
       };
       switch (W) {
-        case 1: match(mttkrp_sparse_match_kernel<1>); break;
-        case 2: match(mttkrp_sparse_match_kernel<2>); break;
-        case 4: match(mttkrp_sparse_match_kernel<4>); break;
-        default: match(mttkrp_sparse_match_kernel<8>); break;
+        case 1: filter(mttkrp_sparse_filter_kernel<1>); break;
+        case 2: filter(mttkrp_sparse_filter_kernel<2>); break;
+        case 4: filter(mttkrp_sparse_filter_kernel<4>); break;
+        default: filter(mttkrp_sparse_filter_kernel<8>); break;
       }
-      // slices with more matches than a staging row holds: the single pass
-      // into their staging rows (the list length stays on the device)
-      {
-        const SparseParams saved = P;
-        P.slice_list = P.ovf_list;
-        P.nlist_dev = P.ovf;
-        STAM_CUDA_CHECK(cudaMemsetAsync(P.tile_counter, 0, sizeof(unsigned long long), call.stream()));
-        launch_single();
-        P = saved;
-      }
-      auto dvals = [&](auto kern) {
-        call.before_launch("mttkrp_sparse_dvals");
-        kern<<<(unsigned)std::min<int64_t>(ceil_div(I, 8), (int64_t)sms * 16), 256, 0, call.stream()>>>(P);
+      // the filter's listed slices: row lengths by the single-pass kernel (list
+      // lengths stay on the device; beside the expansion on a second stream the
+      // kernel's large CTAs cost more residency than the overlap gains:
+      // 5.26 vs 4.89 ms at config 5)
+      launch_list(0, 1, call.stream());
+      auto expand = [&](auto kern) {
+        int per_sm = 1;
+        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+        call.before_launch("mttkrp_sparse_expand");
+        kern<<<(unsigned)std::min<int64_t>(ceil_div(I, 8), (int64_t)std::max(1, per_sm) * sms), 256, 0,
+               call.stream()>>>(P);
         call.after_launch();
       };
       switch (W) {
-        case 1: dvals(mttkrp_sparse_dvals_kernel<1>); break;
-        case 2: dvals(mttkrp_sparse_dvals_kernel<2>); break;
-        case 4: dvals(mttkrp_sparse_dvals_kernel<4>); break;
-        default: dvals(mttkrp_sparse_dvals_kernel<8>); break;
+        case 1: expand(mttkrp_sparse_expand_kernel<1>); break;
+        case 2: expand(mttkrp_sparse_expand_kernel<2>); break;
+        case 4: expand(mttkrp_sparse_expand_kernel<4>); break;
+        default: expand(mttkrp_sparse_expand_kernel<8>); break;
       }
+      launch_list(1, 1, call.stream());
     }
     size_t temp_bytes = 0;
     STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, cpos + 1, cpos + 1, I,
@@ -1947,26 +2066,17 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
     P.out_vals = A->vals;
     if (three) {
       const size_t asmem = ws_bytes * kSpWarps;
-      auto accum = [&](auto kern) {
-        STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-        int per_sm = 1;
-        STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpWarps * 32, asmem));
-        const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
-        call.before_launch("mttkrp_sparse_accum");
-        kern<<<(unsigned)grid, kSpWarps * 32, asmem, call.stream()>>>(P);
-        call.after_launch();
-      };
-      switch (W) {
-        case 1: accum(mttkrp_sparse_accum_kernel<1>); break;
-        case 2: accum(mttkrp_sparse_accum_kernel<2>); break;
-        case 4: accum(mttkrp_sparse_accum_kernel<4>); break;
-        default: accum(mttkrp_sparse_accum_kernel<8>); break;
-      }
-      SparseParams Q = P;
-      Q.slice_list = P.ovf_list;
-      Q.nlist_dev = P.ovf;
-      call.before_launch("mttkrp_sparse_place");
-      mttkrp_sparse_place_kernel<<<(unsigned)sms * 2, 256, 0, call.stream()>>>(Q);
+      STAM_CUDA_CHECK(cudaFuncSetAttribute(mttkrp_sparse_accum_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+      int per_sm = 1;
+      STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mttkrp_sparse_accum_kernel,
+                                                                    kSpWarps * 32, asmem));
+      const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
+      // the listed slices again, now straight into their CSR rows
+      launch_list(0, 2, call.stream());
+      launch_list(1, 2, call.stream());
+      call.before_launch("mttkrp_sparse_accum");
+      mttkrp_sparse_accum_kernel<<<(unsigned)grid, kSpWarps * 32, asmem, call.stream()>>>(P);
       call.after_launch();
     } else {
       call.before_launch("mttkrp_sparse_compact");

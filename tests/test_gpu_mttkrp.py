@@ -96,6 +96,49 @@ def test_mttkrp_sparse_multi_nonzero_fibers(ctx):
     oracle.compare_csr(A, oracle.mttkrp_sparse(B, C, D))
 
 
+@pytest.mark.parametrize("per_row,sizes", [(6, 60), (24, 60), (3, 400), (40, 12)])
+def test_mttkrp_sparse_three_phase_edges(ctx, per_row, sizes):
+    # mostly single-nonzero fibers (the three-phase path) with some longer
+    # fibers among them: sparse factors (few matches), dense factors (more hits
+    # and matches than a slice's rows hold, columns shared by two nonzeros of
+    # a fiber -> those slices take the single-pass kernel), long slices, and
+    # the SPEC multiplication counter across all of them
+    from paper_1802_10574_b200 import _native as N
+
+    B = G.csf3((300, 6000, 450), np.full(300, sizes, dtype=np.int64), 21)
+    assert B.nnz <= B.nfibers + B.nfibers // 8  # the three-phase path's condition
+    C = G.csr_fixed(6000, 64, per_row, 22)
+    D = G.csr_fixed(450, 64, per_row, 23)
+    st = N.Stats()
+    A = ctx.mttkrp(_d(B), _d(C), _d(D), stats=st)
+    oracle.compare_csr(A, oracle.mttkrp_sparse(B, C, D))
+    assert st.mults == oracle.last_counters()["mults"]
+
+
+def test_mttkrp_sparse_empty_slices_and_unaligned_views(ctx):
+    # slices without fibers (leading, trailing, in runs) and CSF arrays that do
+    # not start on a 16-byte boundary (bulk copies are replaced by lane copies)
+    import torch
+
+    sizes = np.zeros(257, dtype=np.int64)
+    sizes[[3, 4, 40, 41, 42, 200]] = [70, 1, 33, 64, 5, 90]
+    B = G.csf3((257, 300, 310), sizes, 31)
+    C = G.csr_fixed(300, 128, 8, 32)
+    D = G.csr_fixed(310, 128, 8, 33)
+    want = oracle.mttkrp_sparse(B, C, D)
+    oracle.compare_csr(ctx.mttkrp(_d(B), _d(C), _d(D)), want)
+
+    def shifted(a):
+        buf = torch.empty(len(a) + 1, dtype=torch.from_numpy(a).dtype, device="cuda")
+        buf[1:].copy_(torch.from_numpy(a))
+        return buf[1:]
+
+    Bd = _d(B)
+    Bu = type(Bd)(Bd.dims, Bd.pos1, shifted(B.idx1), shifted(B.pos2), shifted(B.idx2), shifted(B.vals))
+    assert Bu.idx1.data_ptr() % 16 == 8
+    oracle.compare_csr(ctx.mttkrp(Bu, _d(C), _d(D)), want)
+
+
 def test_mttkrp_sparse_matches_dense_where_present(ctx):
     rng = np.random.default_rng(2)
     t = rng.random((5, 6, 7)) * (rng.random((5, 6, 7)) < 0.4)
