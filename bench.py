@@ -716,7 +716,7 @@ def run_reference(args, cid):
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -857,7 +857,29 @@ def run_config(W, args, ctx, stream, world, rank, dist_on, local, cpu_target_s):
     return res
 
 
+# The contract is ONE JSON line on stdout.  Libraries print there too (NCCL
+# writes its version banner to stdout when the communicator is created), so the
+# process's stdout is pointed at stderr for the whole run and the line goes to
+# a private duplicate of the original descriptor.
+_OUT = None
+
+
+def _capture_stdout():
+    global _OUT
+    if _OUT is None:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def _emit(line):
+    out = _OUT if _OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    _capture_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
@@ -951,7 +973,7 @@ def main():
         if len(cids) > 1:
             line["configs"] = {str(c): {k: v for k, v in r.items() if k != "clocks"}
                                for c, r in results.items()}
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if dist_on:
         dist.destroy_process_group()
     ctx.close()

@@ -610,8 +610,6 @@ struct SparseParams {
   const unsigned long long* nlist_dev;  // list length on the device (overrides nlist)
   unsigned long long* ovf;     // [0] overflowed slices (appended to ovf_list)
   int64_t* ovf_list;
-  unsigned long long* ovf2;    // the same, filled by the expansion phase
-  int64_t* ovf_list2;
   int tma_ok;                  // the CSF arrays sit on 16-byte boundaries (bulk copies)
 };
 
@@ -1418,7 +1416,7 @@ __global__ void __launch_bounds__(256) mttkrp_sparse_expand_kernel(const SparseP
     if (ovf) {
       if (lane == 0) {
         P.rec_cnt[i] = -1;
-        P.ovf_list2[atomicAdd(P.ovf2, 1ull)] = i;
+        P.ovf_list[atomicAdd(P.ovf, 1ull)] = i;
       }
     } else {
       const int cnt = warp_sum(__popc(pres[wl][lane]));
@@ -1967,13 +1965,13 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       }
     };
     // the single-pass kernel over one of the slice lists of the three-phase path
-    auto launch_list = [&](int which, int mode, cudaStream_t st) {
+    auto launch_list = [&](int mode, cudaStream_t st) {
       const SparseParams saved = P;
-      P.slice_list = which == 0 ? saved.ovf_list : saved.ovf_list2;
-      P.nlist_dev = which == 0 ? saved.ovf : saved.ovf2;
+      P.slice_list = saved.ovf_list;
+      P.nlist_dev = saved.ovf;
       P.mode = mode;
       if (mode == 2) P.mults = nullptr;  // counted by the first run
-      P.tile_counter = reinterpret_cast<unsigned long long*>(ctl + 4 + which + 2 * (mode == 2));
+      P.tile_counter = reinterpret_cast<unsigned long long*>(ctl + 4 + mode);
       launch_single(st);
       P = saved;
     };
@@ -2001,12 +1999,9 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       P.rec_cnt = call.scratch_n<int32_t>((size_t)I);
       P.mat_cnt = call.scratch_n<int32_t>((size_t)I);
       P.dsum = reinterpret_cast<uint32_t*>(call.scratch_n<int32_t>((size_t)I));
-      // slices left to the single-pass kernel: listed by the filter (list 1)
-      // and by the expansion (list 2), so list 1 can be evaluated beside it
+      // slices left to the single-pass kernel (listed by the filter and by the expansion)
       P.ovf = reinterpret_cast<unsigned long long*>(ctl + 2);
-      P.ovf2 = reinterpret_cast<unsigned long long*>(ctl + 3);
-      P.ovf_list = call.scratch_n<int64_t>((size_t)(2 * I));
-      P.ovf_list2 = P.ovf_list + I;
+      P.ovf_list = call.scratch_n<int64_t>((size_t)I);
       auto aligned16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
       P.tma_ok = aligned16(P.idx1) && aligned16(P.pos2) && aligned16(P.idx2) && aligned16(P.vals) &&
                  std::getenv("STAM_SP_NO_TMA") == nullptr;
@@ -2027,11 +2022,6 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
         case 4: filter(mttkrp_sparse_filter_kernel<4>); break;
         default: filter(mttkrp_sparse_filter_kernel<8>); break;
       }
-      // the filter's listed slices: row lengths by the single-pass kernel (list
-      // lengths stay on the device; beside the expansion on a second stream the
-      // kernel's large CTAs cost more residency than the overlap gains:
-      // 5.26 vs 4.89 ms at config 5)
-      launch_list(0, 1, call.stream());
       auto expand = [&](auto kern) {
         int per_sm = 1;
         STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
@@ -2046,7 +2036,11 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
         case 4: expand(mttkrp_sparse_expand_kernel<4>); break;
         default: expand(mttkrp_sparse_expand_kernel<8>); break;
       }
-      launch_list(1, 1, call.stream());
+      // the listed slices: row lengths by the single-pass kernel (the list length
+      // stays on the device; beside the expansion on a second stream the
+      // kernel's large CTAs cost more residency than the overlap gains:
+      // 5.26 vs 4.89 ms at config 5)
+      launch_list(1, call.stream());
     }
     size_t temp_bytes = 0;
     STAM_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, cpos + 1, cpos + 1, I,
@@ -2073,8 +2067,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
                                                                     kSpWarps * 32, asmem));
       const int64_t grid = std::min<int64_t>(ceil_div(I, kSpWarps), (int64_t)std::max(1, per_sm) * sms);
       // the listed slices again, now straight into their CSR rows
-      launch_list(0, 2, call.stream());
-      launch_list(1, 2, call.stream());
+      launch_list(2, call.stream());
       call.before_launch("mttkrp_sparse_accum");
       mttkrp_sparse_accum_kernel<<<(unsigned)grid, kSpWarps * 32, asmem, call.stream()>>>(P);
       call.after_launch();
