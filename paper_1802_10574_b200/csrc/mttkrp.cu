@@ -1477,7 +1477,7 @@ __global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(cons
         const bool on = t0 + u * 32 + lane < n;
         cv[u] = on ? ld_keep(P.cvals + m[u].c, keep) : 0.0;
         dv[u] = on ? ld_keep(P.dvals + m[u].d, keep) : 0.0;
-        b[u] = on ? hrow[m[u].meta >> 10].b : 0.0;
+        b[u] = on ? __ldcs(&hrow[m[u].meta >> 10].b) : 0.0;  // streamed like the records
       }
 #pragma unroll
       for (int u = 0; u < kAU; u++)
