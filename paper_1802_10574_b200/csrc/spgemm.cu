@@ -459,10 +459,69 @@ __global__ void tiny_numeric_kernel(const SpgemmParams P, const int64_t* rows, i
 // them; each lane keeps its own A-entry cursor and issues kBatch independent
 // (idx, val) gathers before consuming them.  f(col, value) sees every product
 // exactly once; kNumeric false skips the value loads.
+// One batch of NW windows of 32 products starting at `base` (uniform) of the
+// warp's range [.., w1): lane's product in window u is base + 32u + lane.
+// q[u] = its B entry, av[u] = its A value, ok[u] = inside the range.  pb / ob
+// (the A entry holding product `base` and that entry's first product) are
+// advanced to the batch's end.
+template <bool kNumeric, int NW>
+__device__ __forceinline__ void product_windows(const SpgemmParams& P, int64_t a0, int na, int total,
+                                                const int* aoff, int base, int w1, int& pb, int& ob,
+                                                int64_t (&q)[NW], double (&av)[NW], bool (&ok)[NW]) {
+  const int lane = (int)lane_id();
+  const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+#pragma unroll
+  for (int u = 0; u < NW; u++) {
+    const int wb = base + 32 * u;  // window start (uniform)
+    const int j = wb + lane;
+    ok[u] = j < w1;
+    q[u] = 0;
+    av[u] = 0.0;
+    if (wb >= w1) continue;  // uniform
+    // boundaries of the next 32 entries, relative to the window start
+    const int pe = pb + 1 + lane;
+    const int bnd = pe < na ? aoff[pe] - wb : (1 << 30);
+    const int nxt = __shfl_down_sync(kFull, bnd, 1);
+    const bool empty_seg = lane < 31 && bnd == nxt && bnd <= 32;
+    int p, op;
+    if (!__any_sync(kFull, empty_seg)) {
+      // lane's entry = pb + #boundaries at or below it (all boundaries >= 1)
+      const unsigned M = __reduce_or_sync(kFull, bnd < 32 ? (1u << bnd) : 0u);
+      const int c = __popc(M & upto);
+      p = pb + c;
+      const int bc = __shfl_sync(kFull, bnd, (c + 31) & 31);
+      op = c == 0 ? ob : bc + wb;
+      // advance to the entry holding product wb + 32
+      const int adv = __popc(M) + (__any_sync(kFull, bnd == 32) ? 1 : 0);
+      if (adv > 0) {
+        const int ba = __shfl_sync(kFull, bnd, adv - 1);
+        pb += adv;
+        ob = ba + wb;
+      }
+    } else {
+      // rows with empty B rows in this window: per-lane cursor
+      p = pb;
+      if (ok[u])
+        while (p + 1 < na && aoff[p + 1] <= j) p++;
+      op = aoff[p];
+      const int last = min(wb + 32, total) - 1;
+      int pn = pb;
+      while (pn + 1 < na && aoff[pn + 1] <= last) pn++;
+      // entry holding product wb + 32 (or the last one)
+      while (pn + 1 < na && aoff[pn + 1] <= wb + 32) pn++;
+      pb = __shfl_sync(kFull, pn, 0);
+      ob = aoff[pb];
+    }
+    if (ok[u]) {
+      q[u] = P.bst[a0 + p] + (j - op);
+      if (kNumeric) av[u] = P.avals[a0 + p];
+    }
+  }
+}
+
 template <bool kNumeric, typename F>
 __device__ __forceinline__ void for_products(const SpgemmParams& P, int64_t a0, int na, int total,
                                              F f) {
-  const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int per = (total + nwarps - 1) / nwarps;
@@ -472,58 +531,11 @@ __device__ __forceinline__ void for_products(const SpgemmParams& P, int64_t a0, 
   // pb: A entry holding product `base`; ob: its first product (aoff[pb])
   int pb = entry_of_warp(aoff, na, w0);
   int ob = aoff[pb];
-  const unsigned upto = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
   for (int base = w0; base < w1; base += 32 * kBatch) {
     int64_t q[kBatch];
     double av[kBatch];
     bool ok[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; u++) {
-      const int wb = base + 32 * u;  // window start (uniform)
-      const int j = wb + lane;
-      ok[u] = j < w1;
-      q[u] = 0;
-      av[u] = 0.0;
-      if (wb >= w1) continue;  // uniform
-      // boundaries of the next 32 entries, relative to the window start
-      const int pe = pb + 1 + lane;
-      const int bnd = pe < na ? aoff[pe] - wb : (1 << 30);
-      const int nxt = __shfl_down_sync(kFull, bnd, 1);
-      const bool empty_seg = lane < 31 && bnd == nxt && bnd <= 32;
-      int p, op;
-      if (!__any_sync(kFull, empty_seg)) {
-        // lane's entry = pb + #boundaries at or below it (all boundaries >= 1)
-        const unsigned M = __reduce_or_sync(kFull, bnd < 32 ? (1u << bnd) : 0u);
-        const int c = __popc(M & upto);
-        p = pb + c;
-        const int bc = __shfl_sync(kFull, bnd, (c + 31) & 31);
-        op = c == 0 ? ob : bc + wb;
-        // advance to the entry holding product wb + 32
-        const int adv = __popc(M) + (__any_sync(kFull, bnd == 32) ? 1 : 0);
-        if (adv > 0) {
-          const int ba = __shfl_sync(kFull, bnd, adv - 1);
-          pb += adv;
-          ob = ba + wb;
-        }
-      } else {
-        // rows with empty B rows in this window: per-lane cursor
-        p = pb;
-        if (ok[u])
-          while (p + 1 < na && aoff[p + 1] <= j) p++;
-        op = aoff[p];
-        const int last = min(wb + 32, total) - 1;
-        int pn = pb;
-        while (pn + 1 < na && aoff[pn + 1] <= last) pn++;
-        // entry holding product wb + 32 (or the last one)
-        while (pn + 1 < na && aoff[pn + 1] <= wb + 32) pn++;
-        pb = __shfl_sync(kFull, pn, 0);
-        ob = aoff[pb];
-      }
-      if (ok[u]) {
-        q[u] = P.bst[a0 + p] + (j - op);
-        if (kNumeric) av[u] = P.avals[a0 + p];
-      }
-    }
+    product_windows<kNumeric, kBatch>(P, a0, na, total, aoff, base, w1, pb, ob, q, av, ok);
     int64_t col[kBatch];
     double bv[kBatch];
 #pragma unroll
@@ -825,9 +837,11 @@ template <int THREADS, int TB>
 __global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 ? 32 : 1536 / THREADS)) hash_numeric_kernel(const SpgemmParams P,
                                                                 const int64_t* rows,
                                                                 int64_t nrows,
-                                                                unsigned long long* claim) {
+                                                                unsigned long long* claim,
+                                                                const unsigned long long* nrows_dev) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   HashSmem<TB>& S = *reinterpret_cast<HashSmem<TB>*>(smem_raw);
+  if (nrows_dev) nrows = (int64_t)*nrows_dev;  // a list built on the device
   RowClaims<THREADS> rc(claim, &S.claimed);
   while (true) {
     const int64_t r = rc.next();
@@ -861,6 +875,202 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 
     // rank the runs (mutually ordered) and write the row in column order
     drain_table<THREADS>(S.keys, P.values ? S.vals : nullptr, nslots, sm.c0, P.cidx + dst,
                          P.cvals + dst, S.scan, P.sorted);
+    rc.publish();
+    cta_sync<THREADS>();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Numeric pass of the hash tiers by bucketed counting sort.  The hash tables
+// above are at most half full and followed by an overflow region, so their
+// sorted drain walks ~4.3 slots per product (~45 % of the numeric kernels'
+// instructions); the exact row length is known from the symbolic pass, so the
+// numeric pass does not need a table at all:
+//   * every thread keeps its (at most PER) products in registers;
+//   * a product's bucket is its column scaled into ~total/4 order-preserving
+//     buckets (the hash tiers' slot map); an atomic per product counts the
+//     bucket and gives the product its place in it;
+//   * a block scan turns counts into bases, the products are staged bucket
+//     by bucket in shared memory (work proportional to the products, not to a
+//     table);
+//   * inside a bucket (4 entries on average) an entry is the representative
+//     of its column if no earlier entry holds it; representatives are ranked
+//     among their bucket's representatives, add their duplicates' values in
+//     stage order, and go to their final position through a second staging
+//     buffer, so the row leaves in coalesced stores.
+// A row with a bucket of more than kBucketMax entries (clustered columns: the
+// in-bucket work is quadratic) is listed for the hash kernel.
+constexpr int kBucketMax = 48;
+
+template <int THREADS, int PER>
+struct BucketSmem {
+  int cnt[THREADS + 1];   // entries per bucket, then exclusive bases (cnt[nb] = total)
+  int ucnt[THREADS + 1];  // representatives per bucket, then exclusive bases
+  uint32_t col[THREADS * PER];
+  double val[THREADS * PER];
+  uint32_t ocol[THREADS * PER];
+  double oval[THREADS * PER];
+  unsigned char rep[THREADS * PER];
+  int scan[33];
+  int64_t claimed;
+};
+
+template <int THREADS>
+__device__ __forceinline__ int cta_exclusive_scan(int v, int* sh) {
+  if constexpr (THREADS == 32) {
+    return warp_inclusive_scan(v) - v;
+  } else {
+    return block_exclusive_scan(v, sh, nullptr);
+  }
+}
+
+template <int THREADS, int PER>
+__global__ void __launch_bounds__(THREADS, (THREADS == 1024 ? 1 : THREADS == 32 ? 32 : 1536 / THREADS))
+    bucket_numeric_kernel(const SpgemmParams P, const int64_t* rows, int64_t nrows, unsigned long long* claim,
+                          unsigned long long* fb_count, int64_t* fb_rows) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Smem = BucketSmem<THREADS, PER>;
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  constexpr int kWarpsN = THREADS / 32;
+  RowClaims<THREADS> rc(claim, &S.claimed);
+  while (true) {
+    const int64_t r = rc.next();
+    if (r >= nrows) break;
+    const int64_t i = rows[r];
+    const int64_t dst = P.cpos[i];
+    const int total = (int)P.prod[i];
+    const int64_t a0 = P.apos[i];
+    const int na = (int)(P.apos[i + 1] - a0);
+    // ~total/4 buckets, a power of two, at most one per thread
+    int nb = total <= 4 ? 1 : (1 << (32 - __clz(total - 1))) >> 2;
+    nb = min(nb, THREADS);
+    const SlotMap sm = row_slot_map(P, i, nb);
+    if (tid < nb) {
+      S.cnt[tid] = 0;
+      S.ucnt[tid] = 0;
+    }
+    cta_sync<THREADS>();
+    // the thread's products (one batch of PER windows per warp covers the row)
+    uint32_t col[PER];
+    double val[PER];
+    bool ok[PER];
+    int bk[PER], ix[PER];
+    {
+      const int per = (total + kWarpsN - 1) / kWarpsN;  // <= 32 * PER
+      const int w0 = min(total, warp * per), w1 = min(total, w0 + per);
+      int64_t q[PER];
+      double av[PER];
+#pragma unroll
+      for (int u = 0; u < PER; u++) {
+        ok[u] = false;
+        q[u] = 0;
+        av[u] = 0.0;
+      }
+      if (w0 < w1) {
+        const int* aoff = P.aoff + a0;
+        int pb = entry_of_warp(aoff, na, w0);
+        int ob = aoff[pb];
+        if (P.values)
+          product_windows<true, PER>(P, a0, na, total, aoff, w0, w1, pb, ob, q, av, ok);
+        else
+          product_windows<false, PER>(P, a0, na, total, aoff, w0, w1, pb, ob, q, av, ok);
+      }
+#pragma unroll
+      for (int u = 0; u < PER; u++) {
+        col[u] = 0;
+        val[u] = 0.0;
+        if (ok[u]) {
+          col[u] = (uint32_t)((int64_t)P.bcol32[q[u]] - sm.c0);
+          if (P.values) val[u] = mul_rn(av[u], P.bvals[q[u]]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      bk[u] = 0;
+      ix[u] = 0;
+      if (ok[u]) {
+        bk[u] = min(nb - 1, sm((int64_t)col[u] + sm.c0));
+        ix[u] = atomicAdd(&S.cnt[bk[u]], 1);
+      }
+    }
+    cta_sync<THREADS>();
+    const int mine = tid < nb ? S.cnt[tid] : 0;
+    bool big;
+    if constexpr (THREADS == 32) {
+      big = __any_sync(kFull, mine > kBucketMax);
+    } else {
+      big = __syncthreads_or(mine > kBucketMax ? 1 : 0) != 0;
+    }
+    if (big) {
+      // clustered columns: the hash kernel takes the row
+      if (tid == 0) fb_rows[atomicAdd(fb_count, 1ull)] = i;
+      rc.publish();
+      cta_sync<THREADS>();
+      continue;
+    }
+    {
+      const int excl = cta_exclusive_scan<THREADS>(mine, S.scan);
+      cta_sync<THREADS>();
+      if (tid < nb) S.cnt[tid] = excl;
+      if (tid == 0) S.cnt[nb] = total;
+      cta_sync<THREADS>();
+    }
+#pragma unroll
+    for (int u = 0; u < PER; u++)
+      if (ok[u]) {
+        const int at = S.cnt[bk[u]] + ix[u];
+        S.col[at] = col[u];
+        S.val[at] = val[u];
+      }
+    cta_sync<THREADS>();
+    // representatives: the first entry of its column in the bucket's stage order
+    bool rp[PER];
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+      rp[u] = false;
+      if (ok[u]) {
+        const int lo = S.cnt[bk[u]], me = lo + ix[u];
+        bool first = true;
+        for (int t = lo; t < me; t++) first &= S.col[t] != col[u];
+        rp[u] = first;
+        S.rep[me] = first ? 1 : 0;
+        if (first) atomicAdd(&S.ucnt[bk[u]], 1);
+      }
+    }
+    cta_sync<THREADS>();
+    {
+      const int umine = tid < nb ? S.ucnt[tid] : 0;
+      const int uex = cta_exclusive_scan<THREADS>(umine, S.scan);
+      cta_sync<THREADS>();
+      if (tid < nb) S.ucnt[tid] = uex;
+      if (tid == nb - 1) S.ucnt[nb] = uex + umine;  // the row's length
+      cta_sync<THREADS>();
+    }
+    // final position: the bucket's base + the rank among its representatives
+#pragma unroll
+    for (int u = 0; u < PER; u++)
+      if (ok[u] && rp[u]) {
+        const int lo = S.cnt[bk[u]], hi = S.cnt[bk[u] + 1], me = lo + ix[u];
+        int rank = 0;
+        double sum = add_rn(0.0, val[u]);  // the workspace's first insert accumulates into 0.0
+        for (int t = lo; t < hi; t++) {
+          const uint32_t c2 = S.col[t];
+          rank += (S.rep[t] && c2 < col[u]) ? 1 : 0;
+          if (t > me && c2 == col[u]) sum = add_rn(sum, S.val[t]);
+        }
+        const int out = S.ucnt[bk[u]] + rank;
+        S.ocol[out] = col[u];
+        S.oval[out] = sum;
+      }
+    cta_sync<THREADS>();
+    const int len = S.ucnt[nb];
+    for (int t = tid; t < len; t += THREADS) {
+      P.cidx[dst + t] = sm.c0 + (int64_t)S.ocol[t];
+      if (P.values) P.cvals[dst + t] = S.oval[t];
+    }
     rc.publish();
     cta_sync<THREADS>();
   }
@@ -1030,16 +1240,59 @@ void launch_hash(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows,
                  bool numeric, const char* name, unsigned long long* claim,
                  cudaStream_t st = nullptr) {
   if (n == 0) return;
-  const size_t smem = numeric ? sizeof(HashSmem<TB>) : sizeof(HashKeysSmem<TB>);
-  auto kern = numeric ? hash_numeric_kernel<THREADS, TB> : hash_symbolic_kernel<THREADS, TB>;
-  STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 1;
-  STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
-  const int64_t grid = std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
   if (!st) st = call.stream();
-  call.before_launch(name, st);
-  kern<<<(unsigned)grid, THREADS, smem, st>>>(P, rows, n, claim);
-  call.after_launch(st);
+  const size_t smem = numeric ? sizeof(HashSmem<TB>) : sizeof(HashKeysSmem<TB>);
+  auto grid_for = [&](auto kern) {
+    STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    return (unsigned)std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * call.ctx()->num_sms);
+  };
+  if (numeric) {
+    const unsigned grid = grid_for(hash_numeric_kernel<THREADS, TB>);
+    call.before_launch(name, st);
+    hash_numeric_kernel<THREADS, TB><<<grid, THREADS, smem, st>>>(P, rows, n, claim, nullptr);
+    call.after_launch(st);
+  } else {
+    const unsigned grid = grid_for(hash_symbolic_kernel<THREADS, TB>);
+    call.before_launch(name, st);
+    hash_symbolic_kernel<THREADS, TB><<<grid, THREADS, smem, st>>>(P, rows, n, claim);
+    call.after_launch(st);
+  }
+}
+
+// Numeric pass of a hash tier: the bucket kernel, then the hash kernel over
+// the rows it listed (clustered columns; the list length stays on the device).
+// ctl: [0] bucket claims, [1] listed rows, [2] hash claims.
+template <int THREADS, int TB, int PER>
+void launch_bucket(stamrt::Call& call, const SpgemmParams& P, const int64_t* rows, int64_t n,
+                   const char* name, unsigned long long* ctl, int64_t* fb_rows, cudaStream_t st = nullptr) {
+  if (n == 0) return;
+  if (!st) st = call.stream();
+  const int sms = call.ctx()->num_sms;
+  {
+    using Smem = BucketSmem<THREADS, PER>;
+    auto kern = bucket_numeric_kernel<THREADS, PER>;
+    const size_t smem = sizeof(Smem);
+    STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    const int64_t grid = std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * sms);
+    call.before_launch(name, st);
+    kern<<<(unsigned)grid, THREADS, smem, st>>>(P, rows, n, ctl, ctl + 1, fb_rows);
+    call.after_launch(st);
+  }
+  {
+    const size_t smem = sizeof(HashSmem<TB>);
+    auto kern = hash_numeric_kernel<THREADS, TB>;
+    STAM_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    STAM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    const int64_t grid = std::min<int64_t>(n, (int64_t)std::max(1, per_sm) * sms);
+    call.before_launch("spgemm_hash_clustered", st);
+    kern<<<(unsigned)grid, THREADS, smem, st>>>(P, fb_rows, 0, ctl + 2, ctl + 1);
+    call.after_launch(st);
+  }
 }
 
 // Long rows: scratch offsets (products prefix over the long rows), the
@@ -1755,12 +2008,31 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     launch_tiny<8>(call, P, rows_b[kBinTiny8], counts[kBinTiny8], true, aux);
     launch_tiny<16>(call, P, rows_b[kBinTiny16], counts[kBinTiny16], true, aux);
     launch_tiny<32>(call, P, rows_b[kBinTiny32], counts[kBinTiny32], true, aux);
-    launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5, aux);
-    launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6, aux);
-    launch_hash<SPGEMM_M1_NUM_THREADS, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], true, "spgemm_hashM1_numeric", claims + 13);
-    launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
-    launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
-    launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
+    if (std::getenv("STAM_SPGEMM_HASH_NUMERIC") != nullptr || !P.sorted) {
+      // the hash tables' numeric pass (unsorted output keeps the workspace's slot order)
+      launch_hash<32, 128>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], true, "spgemm_hashXS_numeric", claims + 5, aux);
+      launch_hash<64, 512>(call, P, rows_b[kBinHashS], counts[kBinHashS], true, "spgemm_hashS_numeric", claims + 6, aux);
+      launch_hash<SPGEMM_M1_NUM_THREADS, 1024>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], true, "spgemm_hashM1_numeric", claims + 13);
+      launch_hash<256, 2048>(call, P, rows_b[kBinHashM], counts[kBinHashM], true, "spgemm_hashM_numeric", claims + 7);
+      launch_hash<512, 4096>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], true, "spgemm_hashL1_numeric", claims + 11);
+      launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
+    } else {
+      // bucketed counting sort (rows with clustered columns fall back to the hash kernel)
+      auto* bctl = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 3 * 6));
+      auto* fb = call.scratch_n<int64_t>((size_t)std::max<int64_t>(m, 1));
+      int64_t fo = 0;
+      auto fb_at = [&](int bin) {
+        int64_t* q = fb + fo;
+        fo += (int64_t)counts[bin];
+        return q;
+      };
+      launch_bucket<32, 128, 2>(call, P, rows_b[kBinHashXS], counts[kBinHashXS], "spgemm_bucketXS_numeric", bctl + 0, fb_at(kBinHashXS), aux);
+      launch_bucket<64, 512, 4>(call, P, rows_b[kBinHashS], counts[kBinHashS], "spgemm_bucketS_numeric", bctl + 3, fb_at(kBinHashS), aux);
+      launch_bucket<128, 1024, 4>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], "spgemm_bucketM1_numeric", bctl + 6, fb_at(kBinHashM1));
+      launch_bucket<256, 2048, 4>(call, P, rows_b[kBinHashM], counts[kBinHashM], "spgemm_bucketM_numeric", bctl + 9, fb_at(kBinHashM));
+      launch_bucket<512, 4096, 4>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], "spgemm_bucketL1_numeric", bctl + 12, fb_at(kBinHashL1));
+      launch_bucket<1024, 8192, 4>(call, P, rows_b[kBinHashL], counts[kBinHashL], "spgemm_bucketL_numeric", bctl + 15, fb_at(kBinHashL));
+    }
     call.join();
     const int64_t nnz = defer_nnz ? call.read_scalar(P.cpos + m) : cap;
 
