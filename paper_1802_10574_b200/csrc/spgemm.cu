@@ -2030,8 +2030,16 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
       launch_bucket<64, 512, 4>(call, P, rows_b[kBinHashS], counts[kBinHashS], "spgemm_bucketS_numeric", bctl + 3, fb_at(kBinHashS), aux);
       launch_bucket<128, 1024, 4>(call, P, rows_b[kBinHashM1], counts[kBinHashM1], "spgemm_bucketM1_numeric", bctl + 6, fb_at(kBinHashM1));
       launch_bucket<256, 2048, 4>(call, P, rows_b[kBinHashM], counts[kBinHashM], "spgemm_bucketM_numeric", bctl + 9, fb_at(kBinHashM));
-      launch_bucket<512, 4096, 4>(call, P, rows_b[kBinHashL1], counts[kBinHashL1], "spgemm_bucketL1_numeric", bctl + 12, fb_at(kBinHashL1));
-      launch_bucket<1024, 8192, 4>(call, P, rows_b[kBinHashL], counts[kBinHashL], "spgemm_bucketL_numeric", bctl + 15, fb_at(kBinHashL));
+      #ifndef SPGEMM_BUCKET_L1_THREADS
+#define SPGEMM_BUCKET_L1_THREADS 512
+#endif
+      launch_bucket<SPGEMM_BUCKET_L1_THREADS, 4096, 2048 / SPGEMM_BUCKET_L1_THREADS>(
+          call, P, rows_b[kBinHashL1], counts[kBinHashL1], "spgemm_bucketL1_numeric", bctl + 12, fb_at(kBinHashL1));
+      #ifndef SPGEMM_BUCKET_L_THREADS
+#define SPGEMM_BUCKET_L_THREADS 1024
+#endif
+      launch_bucket<SPGEMM_BUCKET_L_THREADS, 8192, 4096 / SPGEMM_BUCKET_L_THREADS>(
+          call, P, rows_b[kBinHashL], counts[kBinHashL], "spgemm_bucketL_numeric", bctl + 15, fb_at(kBinHashL));
     }
     call.join();
     const int64_t nnz = defer_nnz ? call.read_scalar(P.cpos + m) : cap;
