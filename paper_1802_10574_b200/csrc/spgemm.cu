@@ -2001,6 +2001,10 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
     P.cvals = Cr->vals;
     if (!P.values && cap > 0)  // ASSEMBLE: index only, values defined as zero
       STAM_CUDA_CHECK(cudaMemsetAsync(Cr->vals, 0, sizeof(double) * (size_t)cap, call.stream()));
+    // control words and row lists of the bucketed numeric pass (zeroed on the
+    // main stream before the fork: the auxiliary stream's kernels read them)
+    auto* bctl = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 3 * 6));
+    auto* fb = call.scratch_n<int64_t>((size_t)std::max<int64_t>(m, 1));
     // numeric (ASSEMBLE: the same passes without values): the long-row copy
     // and the small-row tiers on the auxiliary stream
     aux = call.fork();
@@ -2018,8 +2022,6 @@ extern "C" int stam_cuda_spgemm(stam_cuda_ctx* ctx, const stam_csr_view* A, cons
       launch_hash<1024, 8192>(call, P, rows_b[kBinHashL], counts[kBinHashL], true, "spgemm_hashL_numeric", claims + 8);
     } else {
       // bucketed counting sort (rows with clustered columns fall back to the hash kernel)
-      auto* bctl = static_cast<unsigned long long*>(call.scratch_zero(sizeof(unsigned long long) * 3 * 6));
-      auto* fb = call.scratch_n<int64_t>((size_t)std::max<int64_t>(m, 1));
       int64_t fo = 0;
       auto fb_at = [&](int bin) {
         int64_t* q = fb + fo;

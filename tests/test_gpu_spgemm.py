@@ -92,6 +92,41 @@ def test_spgemm_heavy_collisions(ctx):
     oracle.compare_csr(C, oracle.spgemm(A, B))
 
 
+def test_spgemm_clustered_columns_and_duplicates(ctx):
+    # the numeric pass sorts a row's products by order-preserving buckets of its
+    # column span: rows whose columns cluster (one far outlier stretches the
+    # span, so everything else shares a bucket) must fall back to the hash
+    # kernel, and duplicates inside ordinary buckets must fold into one entry
+    n = 1_000_000
+    rows_b, cols_b = [], []
+    for k in range(10):  # B rows 0..9: 30 consecutive columns each
+        rows_b += [k] * 30
+        cols_b += list(range(k * 30, k * 30 + 30))
+    rows_b += [10]
+    cols_b += [n - 1]  # B row 10: the outlier
+    rows_b += [11] * 30
+    cols_b += list(range(0, 30))  # B row 11 repeats row 0's columns
+    for k in range(12, 40):  # B rows 12..39: 40 consecutive columns each, 20 apart (overlapping)
+        rows_b += [k] * 40
+        cols_b += list(range(5000 + (k - 12) * 20, 5000 + (k - 12) * 20 + 40))
+    rng = np.random.default_rng(7)
+    pos_b = np.zeros(41, dtype=np.int64)
+    np.add.at(pos_b, np.asarray(rows_b) + 1, 1)
+    pos_b = np.cumsum(pos_b)
+    B = CSR(40, n, pos_b, np.asarray(cols_b, dtype=np.int64), rng.uniform(-1, 1, len(cols_b)))
+    a_rows = [list(range(11)),        # 301 products, 300 of them in one bucket -> hash kernel
+              [0, 10, 11],            # 61 products, 30 duplicated, clustered
+              [0, 11],                # 60 products over 30 columns: duplicates in every bucket
+              list(range(12, 40)),    # 1120 products, every column held twice (overlapping rows)
+              list(range(0, 40))]     # 1481 products, everything at once
+    pos_a = np.zeros(len(a_rows) + 1, dtype=np.int64)
+    pos_a[1:] = np.cumsum([len(r) for r in a_rows])
+    idx_a = np.concatenate([np.asarray(r, dtype=np.int64) for r in a_rows])
+    A = CSR(len(a_rows), 40, pos_a, idx_a, rng.uniform(-1, 1, len(idx_a)))
+    C = ctx.spgemm(_d(A), _d(B))
+    oracle.compare_csr(C, oracle.spgemm(A, B))
+
+
 def test_spgemm_tiny_rows_bit_exact(ctx):
     A = G.csr_fixed(2000, 3000, 3, 31)
     B = G.csr_fixed(3000, 50, 8, 32)  # <= 24 products per row, many collisions
