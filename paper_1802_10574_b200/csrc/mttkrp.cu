@@ -1318,8 +1318,11 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
 #define SPX_U 1
 #endif
 constexpr int kXU = SPX_U;
+#ifndef SPX_MINB
+#define SPX_MINB 1
+#endif
 template <int W>
-__global__ void __launch_bounds__(256) mttkrp_sparse_expand_kernel(const SparseParams P) {
+__global__ void __launch_bounds__(256, SPX_MINB) mttkrp_sparse_expand_kernel(const SparseParams P) {
   __shared__ uint32_t pres[8][32];
   const int lane = (int)lane_id();
   const int wl = threadIdx.x >> 5;
@@ -1440,7 +1443,10 @@ __global__ void __launch_bounds__(256) mttkrp_sparse_expand_kernel(const SparseP
 #define SPA_U 4
 #endif
 constexpr int kAU = SPA_U;
-__global__ void __launch_bounds__(kSpWarps * 32) mttkrp_sparse_accum_kernel(const SparseParams P) {
+#ifndef SPA_MINB
+#define SPA_MINB 1
+#endif
+__global__ void __launch_bounds__(kSpWarps * 32, SPA_MINB) mttkrp_sparse_accum_kernel(const SparseParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = (int)lane_id();
   const int warp = threadIdx.x >> 5;
