@@ -115,6 +115,21 @@ def test_mttkrp_sparse_three_phase_edges(ctx, per_row, sizes):
     assert st.mults == oracle.last_counters()["mults"]
 
 
+@pytest.mark.parametrize("R", [40, 320, 512])
+def test_mttkrp_sparse_three_phase_ranks(ctx, R):
+    # ranks off the 64-column word boundary and the widest bitmaps (8 words)
+    from paper_1802_10574_b200 import _native as N
+
+    B = G.csf3((400, 3000, 2500), np.full(400, 150, dtype=np.int64), 51)
+    assert B.nnz <= B.nfibers + B.nfibers // 8
+    C = G.csr_fixed(3000, R, max(3, R // 20), 52)
+    D = G.csr_fixed(2500, R, max(3, R // 20), 53)
+    st = N.Stats()
+    A = ctx.mttkrp(_d(B), _d(C), _d(D), stats=st)
+    oracle.compare_csr(A, oracle.mttkrp_sparse(B, C, D))
+    assert st.mults == oracle.last_counters()["mults"]
+
+
 def test_mttkrp_sparse_empty_slices_and_unaligned_views(ctx):
     # slices without fibers (leading, trailing, in runs) and CSF arrays that do
     # not start on a 16-byte boundary (bulk copies are replaced by lane copies)
