@@ -1161,6 +1161,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
     int nrec = 0;
     bool ovf = false;
     unsigned mcur = 0;  // the lane's share of the current slice's sum of |D_k|
+    HitRec* hrow = P.hits + i0 * P.hit_cap;  // the current slice's hit row
     for (uint32_t q = base; q < base + nch; q++) {
       const int s1 = (int)(q & (kMD1 - 1)), s2 = (int)(q & (kMD2 - 1));
       mbar_wait(&Q.bar2[s2], (q / kMD2) & 1u);
@@ -1253,7 +1254,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
               ovf = true;  // the slice goes to the single-pass kernel
             } else {
               if (in_seg && nh > 0) {
-                HitRec* row = P.hits + (i0 + si) * P.hit_cap + nrec + before;
+                HitRec* row = hrow + nrec + before;
                 HitRec rec;
                 rec.j = j;
                 rec.k = k;
@@ -1290,6 +1291,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
           }
           mcur = 0;
           si++;
+          hrow += P.hit_cap;
           fcur = cur_f1;
           cur_f1 = __shfl_sync(kFull, p1r, min(si + 1, 31));
           nrec = 0;
