@@ -1312,14 +1312,12 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
   }
 }
 
-// Phase 2: lanes over the slice's hits, kXU hits per lane and step (their
-// record, bitmap and row-start loads in flight together).  Each hit's shared
-// columns become match records; the slice's distinct columns give its row
-// length in A.
-#ifndef SPX_U
-#define SPX_U 1
-#endif
-constexpr int kXU = SPX_U;
+// Phase 2: lanes over the slice's hits (every lane holds one, so the bit walks
+// run on full warps).  Each hit's shared columns become match records; the
+// slice's distinct columns give its row length in A.  The next round's hit
+// records and the next slice's head (its hit count and first records) are
+// loaded before the current round is expanded: the record stream's DRAM
+// latency stays off the chain record -> bitmaps / row starts -> match records.
 #ifndef SPX_MINB
 #define SPX_MINB 1
 #endif
@@ -1332,8 +1330,23 @@ __global__ void __launch_bounds__(256, SPX_MINB) mttkrp_sparse_expand_kernel(con
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t keep = l2_evict_last_policy();
   unsigned long long mults = 0;
+  // a slice's head: its hit count and (whatever the count) the first 32 records of its row
+  auto head = [&](int64_t i, int& n, HitRec& r0) {
+    n = 0;
+    r0.j = r0.k = 0;
+    r0.b = 0.0;
+    if (i < P.I) {
+      n = P.rec_cnt[i];
+      if (lane < P.hit_cap) r0 = ld_rec(P.hits + i * P.hit_cap + lane);
+    }
+  };
+  int n_nxt;
+  HitRec r_nxt;
+  head(warp, n_nxt, r_nxt);
   for (int64_t i = warp; i < P.I; i += nwarps) {
-    const int n = P.rec_cnt[i];
+    const int n = n_nxt;
+    HitRec rec = r_nxt;
+    head(i + nwarps, n_nxt, r_nxt);
     if (n < 0) continue;  // evaluated by the single-pass kernel
     if (n == 0) {
       // no hit: an empty row; the multiplications that found nothing still count
@@ -1349,73 +1362,58 @@ __global__ void __launch_bounds__(256, SPX_MINB) mttkrp_sparse_expand_kernel(con
     __syncwarp();
     int nmat = 0;
     bool ovf = false;
-    for (int t0 = 0; t0 < n; t0 += 32 * kXU) {
-      HitRec rec[kXU];
-      unsigned long long bc[kXU][W], bd[kXU][W];
-      int64_t d0[kXU], c0[kXU];
-      int x[kXU];
+    for (int t0 = 0; t0 < n; t0 += 32) {
+      const int t = t0 + lane;
+      // the next round's records
+      HitRec rnext;
+      rnext.j = rnext.k = 0;
+      rnext.b = 0.0;
+      if (t + 32 < n) rnext = ld_rec(hrow + t + 32);
+      unsigned long long bc[W], bd[W];
 #pragma unroll
-      for (int u = 0; u < kXU; u++) {
-        const int t = t0 + u * 32 + lane;
-        rec[u].j = rec[u].k = 0;
-        rec[u].b = 0.0;
-        if (t < n) rec[u] = ld_rec(hrow + t);
+      for (int w = 0; w < W; w++) bc[w] = bd[w] = 0ull;
+      int64_t d0 = 0, c0 = 0;
+      int x = 0;
+      if (t < n) {
+        load_bm_keep<W>(P.cbm + (int64_t)rec.j * W, keep, bc);
+        load_bm_keep<W>(P.dbm + (int64_t)rec.k * W, keep, bd);
+        d0 = __ldg(P.dpos + rec.k);
+        c0 = __ldg(P.cpos + rec.j);
+#pragma unroll
+        for (int w = 0; w < W; w++) x += __popcll(bc[w] & bd[w]);
       }
-      int xs = 0;
-#pragma unroll
-      for (int u = 0; u < kXU; u++) {
-        const int t = t0 + u * 32 + lane;
-#pragma unroll
-        for (int w = 0; w < W; w++) bc[u][w] = bd[u][w] = 0ull;
-        d0[u] = c0[u] = 0;
-        if (t < n) {
-          load_bm_keep<W>(P.cbm + (int64_t)rec[u].j * W, keep, bc[u]);
-          load_bm_keep<W>(P.dbm + (int64_t)rec[u].k * W, keep, bd[u]);
-          d0[u] = __ldg(P.dpos + rec[u].k);
-          c0[u] = __ldg(P.cpos + rec[u].j);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kXU; u++) {
-        x[u] = 0;
-#pragma unroll
-        for (int w = 0; w < W; w++) x[u] += __popcll(bc[u][w] & bd[u][w]);
-        xs += x[u];
-      }
-      const int inc = warp_inclusive_scan(xs);
+      const int inc = warp_inclusive_scan(x);
       const int tot = __shfl_sync(kFull, inc, 31);
       if (nmat + tot > P.mat_cap) {
         ovf = true;
         break;
       }
-      MatRec* out = mrow + nmat + inc - xs;
+      if (x > 0) {
+        MatRec* out = mrow + nmat + inc - x;
+        int pc = 0, pd = 0;
 #pragma unroll
-      for (int u = 0; u < kXU; u++) {
-        if (x[u] > 0) {
-          int pc = 0, pd = 0;
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            unsigned long long mm = bc[u][w] & bd[u][w];
-            while (mm) {
-              const int bit = __ffsll((long long)mm) - 1;
-              const unsigned long long below = (1ull << bit) - 1ull;
-              const int rc = pc + __popcll(bc[u][w] & below);
-              const int rd = pd + __popcll(bd[u][w] & below);
-              const unsigned r = (unsigned)(w * 64 + bit);
-              MatRec m;
-              m.c = (int)(c0[u] + rc);
-              m.meta = r | ((unsigned)(t0 + u * 32 + lane) << 10);
-              m.d = d0[u] + rd;
-              st_rec(out++, m);
-              atomicOr(&pres[wl][r >> 5], 1u << (r & 31u));
-              mm &= mm - 1ull;
-            }
-            pc += __popcll(bc[u][w]);
-            pd += __popcll(bd[u][w]);
+        for (int w = 0; w < W; w++) {
+          unsigned long long mm = bc[w] & bd[w];
+          while (mm) {
+            const int bit = __ffsll((long long)mm) - 1;
+            const unsigned long long below = (1ull << bit) - 1ull;
+            const int rc = pc + __popcll(bc[w] & below);
+            const int rd = pd + __popcll(bd[w] & below);
+            const unsigned r = (unsigned)(w * 64 + bit);
+            MatRec m;
+            m.c = (int)(c0 + rc);
+            m.meta = r | ((unsigned)t << 10);
+            m.d = d0 + rd;
+            st_rec(out++, m);
+            atomicOr(&pres[wl][r >> 5], 1u << (r & 31u));
+            mm &= mm - 1ull;
           }
+          pc += __popcll(bc[w]);
+          pd += __popcll(bd[w]);
         }
       }
       nmat += tot;
+      rec = rnext;
     }
     __syncwarp();
     if (ovf) {
