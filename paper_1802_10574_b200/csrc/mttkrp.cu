@@ -19,15 +19,19 @@
 //           are stored directly; slices cut by chunk boundaries leave
 //           per-chunk partials that block sums and a warp per chain add in a
 //           fixed order (deterministic; no atomics on the heavy slices).
-//  sparse — a warp per slice (claimed dynamically), lanes over fibers; per
-//           fiber, w0 is evaluated only at C_j's stored coordinates
-//           (presence-checked; the C_j and D_k column ids are held in
-//           registers and intersected all-pairs); w1 is a dense R-wide
-//           shared-memory workspace with a presence bitmap, drained sorted by
-//           ballot/popcount into a fixed-stride staging row (a row holds <= R
-//           entries); scan + coalesced compaction build the CSR.  (An ordered
-//           look-back made every slice wait for the slowest earlier one: 41% of
-//           warp samples asleep, profiles/r01_ncu_summary.md.)
+//  sparse — three phases whose gathered sets each fit the L2 (see "Three
+//           phases" below): a filter streams the CSF through per-warp shared-
+//           memory rings filled by TMA bulk copies and ANDs the two factor
+//           rows' column bitmaps (a hit record per matching nonzero); an
+//           expansion turns hits into match records on full warps and counts
+//           each slice's distinct columns; after a scan of the row lengths an
+//           accumulation adds w0*C(j,r) into an R-wide shared-memory workspace
+//           with a presence bitmap and drains it sorted (ballot/popcount)
+//           straight into the CSR.  w0 is evaluated only at C's stored
+//           coordinates (presence-checked).  The single-pass kernel (a warp
+//           per slice, matches queued per warp) remains for tensors outside
+//           the three-phase path's limits and for slices that overflow their
+//           record rows.
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
