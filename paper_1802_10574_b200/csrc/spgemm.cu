@@ -16,13 +16,20 @@
 //                                 per warp), one product per lane; distinct
 //                                 rank by a shuffle sweep, values summed in
 //                                 canonical order (bit-exact with the CPU).
-//      hash XS/S/M/L P <= 64/256/1024/4096 : CTA of 1/2/8/32 warps per row with a
-//                                 shared-memory hash table sized 2P whose hash
-//                                 is ORDER-PRESERVING (slot = scaled column,
-//                                 forward linear probing, no wrap): occupied
-//                                 runs are mutually ordered, so sorting the
-//                                 few entries of each run gives the sorted row;
-//                                 values accumulate with shared fp64 atomics.
+//      hash XS/S/M1/M/L1/L P <= 64/256/512/1024/2048/4096 : CTA of 1..32 warps
+//                                 per row.  Symbolic: a shared-memory table of
+//                                 keys sized 2P whose hash is ORDER-PRESERVING
+//                                 (slot = scaled column, forward linear
+//                                 probing, no wrap) counts the distinct
+//                                 columns.  Numeric: bucketed counting sort
+//                                 (bucket_numeric_kernel): products in
+//                                 registers, ~P/4 order-preserving buckets,
+//                                 in-bucket ranks, duplicates folded, coalesced
+//                                 row writes; rows with clustered columns (and
+//                                 unsorted output) use the table's numeric
+//                                 pass, whose occupied runs are mutually
+//                                 ordered (ranked per run in the drain), values
+//                                 accumulated with shared fp64 atomics.
 //      long P > 4096          : 1024-thread CTA per row (rows claimed longest
 //                                 first), a column bitmap over all columns in
 //                                 shared memory (popcount rank) and fp64
