@@ -604,7 +604,7 @@ struct SparseParams {
   // three-phase path: hit and match records per slice
   int32_t* rec_cnt;            // [I] hits of each slice, -1: left to the single-pass kernel
   int32_t* mat_cnt;            // [I] match records of each slice
-  uint32_t* dsum;              // [I] sum of |D_k| over the slice's nonzeros (SPEC counter)
+  unsigned long long* dsum;    // [I] sum of |D_k| over the slice's nonzeros (SPEC counter)
   HitRec* hits;                // [I*hit_cap]
   MatRec* mats;                // [I*mat_cap]
   int32_t hit_cap, mat_cap;
@@ -1150,7 +1150,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
     if (F0r == F1r) {
       if (lane < gcount) {
         P.rec_cnt[i0 + lane] = 0;
-        P.dsum[i0 + lane] = 0u;
+        P.dsum[i0 + lane] = 0ull;
       }
       continue;
     }
@@ -1287,7 +1287,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, SPM_MINB)
             }
           }
           if (cur_f1 > fend) break;  // the slice continues in a later batch
-          const unsigned ds = warp_sum(mcur);
+          const unsigned long long ds = warp_sum((unsigned long long)mcur);
           if (lane == 0) {
             P.rec_cnt[i0 + si] = ovf ? -1 : nrec;
             P.dsum[i0 + si] = ds;
@@ -1430,7 +1430,7 @@ __global__ void __launch_bounds__(256, SPX_MINB) mttkrp_sparse_expand_kernel(con
       if (lane == 0) {
         P.out_pos[i + 1] = cnt;
         P.mat_cnt[i] = nmat;
-        mults += (unsigned long long)P.dsum[i] + (unsigned long long)nmat;
+        mults += P.dsum[i] + (unsigned long long)nmat;
       }
     }
     __syncwarp();
@@ -2008,7 +2008,7 @@ extern "C" int stam_cuda_mttkrp_sparse(stam_cuda_ctx* ctx, const stam_csf3_view*
       P.mats = static_cast<MatRec*>(call.scratch(sizeof(MatRec) * (size_t)I * mat_cap));
       P.rec_cnt = call.scratch_n<int32_t>((size_t)I);
       P.mat_cnt = call.scratch_n<int32_t>((size_t)I);
-      P.dsum = reinterpret_cast<uint32_t*>(call.scratch_n<int32_t>((size_t)I));
+      P.dsum = reinterpret_cast<unsigned long long*>(call.scratch_n<int64_t>((size_t)I));
       // slices left to the single-pass kernel (listed by the filter and by the expansion)
       P.ovf = reinterpret_cast<unsigned long long*>(ctl + 2);
       P.ovf_list = call.scratch_n<int64_t>((size_t)I);
